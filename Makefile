@@ -1,0 +1,54 @@
+# Top-level build: the product library (sm_100a) and the test-only oracle.
+#   make            -> paper_2210_03179_b200/lib/libchebmg_b200.so + oracle/
+#   make lib        -> product only
+CUDA ?= /usr/local/cuda
+NVCC ?= $(CUDA)/bin/nvcc
+CXX ?= g++
+ARCH = -gencode arch=compute_100a,code=sm_100a
+NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -warn-spills \
+          --expt-relaxed-constexpr
+# host code: no -march / -ffast-math (bit-identical seeded inputs)
+CXXFLAGS = -O2 -std=c++20 -fPIC -Wall -Wextra -Wno-unused-parameter -I$(CUDA)/include
+
+SRC = paper_2210_03179_b200/csrc
+OBJ = build/obj
+LIB = paper_2210_03179_b200/lib/libchebmg_b200.so
+
+CU_EXACT = $(SRC)/k_blas.cu $(SRC)/k_fd.cu           # --fmad=false (reference rounding)
+CU_FAST  = $(wildcard $(SRC)/k_sem*.cu)              # FMA on (no reference bits to match)
+CPP      = $(SRC)/capi.cpp $(SRC)/host_setup.cpp $(wildcard $(SRC)/sem*.cpp) $(wildcard $(SRC)/comm*.cpp)
+HDR      = $(wildcard $(SRC)/*.hpp) include/chebmg_b200.h
+
+OBJS = $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_EXACT) $(CU_FAST)) \
+       $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP))
+
+NCCL_LINK ?=   # NCCL is dlopen'ed at run time (comm.cpp)
+
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJ)/k_blas.o $(OBJ)/k_fd.o: $(OBJ)/%.o: $(SRC)/%.cu $(HDR)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) --fmad=false -c $< -o $@
+
+$(OBJ)/k_sem%.o: $(SRC)/k_sem%.cu $(HDR)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJ)/%.o: $(SRC)/%.cpp $(HDR)
+	@mkdir -p $(OBJ)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static $(NCCL_LINK) -lpthread -ldl -lrt
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib oracle clean

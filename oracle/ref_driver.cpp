@@ -1,0 +1,327 @@
+// ref_driver.cpp -- C entry points around the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile straight from the
+// reference headers where they lie (-I /root/reference/proj/include); output
+// goes only to oracle/_ref/libchebmg_ref.so (git-ignored).  Nothing here
+// re-implements reference arithmetic: every numeric result comes from the
+// reference's own templates (chebyshev_smooth, v_cycle, pcg, pgmres,
+// run_case_with, estimate_C).  For the SEM path, which the reference lacks,
+// the oracle's C SEM operator (oracle_sem.c) is wrapped in a class satisfying
+// the reference's LinearOperatorLike concept (operators.hpp:19-26) so that the
+// reference's smoother and Krylov templates drive it -- the CPU baseline the
+// survey prescribes.
+#include <chebmg/harness.hpp>
+#include <chebmg/krylov.hpp>
+#include <chebmg/lanczos.hpp>
+#include <chebmg/multigrid.hpp>
+#include <chebmg/problem.hpp>
+#include <chebmg/smoothers.hpp>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+extern "C" {
+#include "oracle.h"
+}
+
+using namespace chebmg;
+
+namespace {
+
+int classify(const std::exception& e) {
+  if (dynamic_cast<const std::out_of_range*>(&e)) return 2;
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  return 3;
+}
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
+Family fam(int f) {
+  switch (f) {
+    case 0: return Family::first;
+    case 1: return Family::first_opt_lambda;
+    case 2: return Family::fourth;
+    default: return Family::fourth_opt;
+  }
+}
+
+void fill_report(const SolveReport& rep, double* hist, std::size_t hist_cap, std::size_t* hist_len,
+                 std::size_t* its, std::size_t* mv, int* converged, char* status, double* rho,
+                 double* wall) {
+  *hist_len = rep.residual_history.size();
+  for (std::size_t i = 0; i < rep.residual_history.size() && i < hist_cap; ++i)
+    hist[i] = rep.residual_history[i];
+  *its = rep.iterations;
+  *mv = rep.fine_matvecs;
+  *converged = rep.converged ? 1 : 0;
+  std::snprintf(status, 128, "%s", rep.status.c_str());
+  *rho = rep.rho;
+  *wall = rep.wall_time_sec;
+}
+
+// LinearOperatorLike adapter over the oracle's C SEM operator.
+class SemOperator {
+ public:
+  explicit SemOperator(orc_op* op, const orc_sem* s) : op_(op), s_(s) {}
+  std::size_t rows() const { return op_->n; }
+  std::size_t cols() const { return op_->n; }
+  void apply(const Vec& x, Vec& y) const { orc_op_apply(op_, x.data(), y.data()); }
+  Vec diagonal() const {
+    Vec d(op_->n);
+    orc_sem_diagonal(s_, d.data());
+    return d;
+  }
+  std::size_t applications() const { return op_->count; }
+  void reset_applications() const { op_->count = 0; }
+
+ private:
+  orc_op* op_;
+  const orc_sem* s_;
+};
+static_assert(LinearOperatorLike<SemOperator>);
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_random_vector(std::size_t n, std::uint64_t seed, double* out) {
+  const Vec v = random_vector(n, seed);
+  std::memcpy(out, v.data(), n * sizeof(double));
+}
+
+double ref_dot(std::size_t n, const double* a, const double* b) {
+  return dot(Vec(a, a + n), Vec(b, b + n));
+}
+
+void ref_fd_build_problem(std::size_t n, double Lx, double Ly, std::uint64_t seed, double* u,
+                          double* b) {
+  const Problem p = build_problem(Domain(Lx, Ly, n), seed);
+  std::memcpy(u, p.u_exact.data(), p.u_exact.size() * sizeof(double));
+  std::memcpy(b, p.b.data(), p.b.size() * sizeof(double));
+}
+
+void ref_fd_stencil_apply(std::size_t n, double Lx, double Ly, const double* x, double* y) {
+  const StencilOperator A(Domain(Lx, Ly, n));
+  Vec xv(x, x + A.rows()), yv(A.rows());
+  A.apply(xv, yv);
+  std::memcpy(y, yv.data(), yv.size() * sizeof(double));
+}
+
+void ref_fd_prolong(std::size_t n, std::size_t nc, const double* xc, double* y) {
+  const Prolongation P(n, nc);
+  Vec xv(xc, xc + P.coarse_dim()), yv(P.fine_dim());
+  P.apply(xv, yv);
+  std::memcpy(y, yv.data(), yv.size() * sizeof(double));
+}
+
+void ref_fd_restrict(std::size_t n, std::size_t nc, const double* x, double* yc) {
+  const Prolongation P(n, nc);
+  Vec xv(x, x + P.fine_dim()), yv(P.coarse_dim());
+  P.apply_transpose(xv, yv);
+  std::memcpy(yc, yv.data(), yv.size() * sizeof(double));
+}
+
+void* ref_hier_create(std::size_t n, double Lx, double Ly, std::size_t factor,
+                      std::size_t eigen_iterations, std::uint64_t eigen_seed) {
+  try {
+    return new Hierarchy(build_hierarchy(Domain(Lx, Ly, n), factor, eigen_iterations, eigen_seed));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_hier_destroy(void* h) { delete static_cast<Hierarchy*>(h); }
+double ref_hier_lambda(void* h) { return static_cast<Hierarchy*>(h)->lambda_tilde; }
+std::size_t ref_hier_bandwidth(void* h) { return static_cast<Hierarchy*>(h)->coarse->bandwidth(); }
+std::size_t ref_hier_coarse_nnz(void* h) { return static_cast<Hierarchy*>(h)->Ac.nonzeros(); }
+
+void ref_hier_coarse_solve(void* hp, const double* rc, double* ec) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  Vec r(rc, rc + h->P.coarse_dim()), e(h->P.coarse_dim());
+  h->coarse->solve(r, e);
+  std::memcpy(ec, e.data(), e.size() * sizeof(double));
+}
+
+void ref_hier_coarse_apply(void* hp, const double* xc, double* yc) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  Vec x(xc, xc + h->P.coarse_dim()), y(h->P.coarse_dim());
+  h->Ac.apply(x, y);
+  std::memcpy(yc, y.data(), y.size() * sizeof(double));
+}
+
+int ref_smooth(void* hp, int family, std::size_t order, double lambda_tilde, double lmax_mult,
+               double lmin_mult, const double* b, double* x, int x_is_zero, std::size_t* apps) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  return guarded([&] {
+    ChebyshevConfig cfg;
+    cfg.family = fam(family);
+    cfg.lambda_tilde = lambda_tilde;
+    cfg.lambda_max_multiplier = lmax_mult;
+    cfg.lambda_min_multiplier = lmin_mult;
+    const std::size_t n = h->fine_dim();
+    Vec bv(b, b + n), xv(x, x + n);
+    const std::size_t a0 = h->A.applications();
+    chebyshev_smooth(h->A, h->inv_diag, cfg, order, bv, xv, x_is_zero != 0);
+    *apps = h->A.applications() - a0;
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+int ref_v_cycle(void* hp, int family, double lmax_mult, double lmin_mult, std::size_t k_pre,
+                std::size_t k_post, const double* b, double* x, int x_is_zero, std::size_t* apps) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  return guarded([&] {
+    ChebyshevConfig s;
+    s.family = fam(family);
+    s.lambda_tilde = h->lambda_tilde;
+    s.lambda_max_multiplier = lmax_mult;
+    s.lambda_min_multiplier = lmin_mult;
+    const std::size_t n = h->fine_dim();
+    Vec bv(b, b + n), xv(x, x + n);
+    const std::size_t a0 = h->A.applications();
+    v_cycle(*h, CycleConfig{s, k_pre, k_post}, bv, xv, x_is_zero != 0);
+    *apps = h->A.applications() - a0;
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+// driver: 0 pcg, 1 pgmres, 2 mg_solver (stationary)
+int ref_solve(void* hp, int driver, int family, double lmax_mult, double lmin_mult,
+              std::size_t k_pre, std::size_t k_post, const double* b, const double* x0, double tol,
+              std::size_t maxit, std::size_t restart, double* x_out, double* hist,
+              std::size_t hist_cap, std::size_t* hist_len, std::size_t* its, std::size_t* mv,
+              int* converged, char* status, double* rho, double* wall) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  return guarded([&] {
+    ChebyshevConfig s;
+    s.family = fam(family);
+    s.lambda_tilde = h->lambda_tilde;
+    s.lambda_max_multiplier = lmax_mult;
+    s.lambda_min_multiplier = lmin_mult;
+    const CycleConfig cc{s, k_pre, k_post};
+    const Preconditioner M = [&](const Vec& v) { return preconditioner_apply(*h, cc, v); };
+    const std::size_t n = h->fine_dim();
+    const Vec bv(b, b + n), x0v(x0, x0 + n);
+    SolveOptions o;
+    o.tol = tol;
+    o.maxit = maxit;
+    o.restart = restart;
+    SolveReport rep;
+    Vec x(n, 0.0);
+    if (driver == 0) {
+      auto res = pcg(h->A, M, bv, x0v, o);
+      x = res.first;
+      rep = res.second;
+    } else if (driver == 1) {
+      auto res = pgmres(h->A, M, bv, x0v, o);
+      x = res.first;
+      rep = res.second;
+    } else {
+      rep = detail::stationary_solve(h->A, M, bv, tol, maxit);
+    }
+    std::memcpy(x_out, x.data(), n * sizeof(double));
+    fill_report(rep, hist, hist_cap, hist_len, its, mv, converged, status, rho, wall);
+  });
+}
+
+// run_case (harness.hpp:253-258) with the hierarchy reused across calls
+int ref_run_case_with(void* hp, double Lx, std::size_t n, std::size_t factor, int family,
+                      std::size_t k, int cycle, int driver, double tol, std::size_t restart,
+                      std::size_t maxit, double* hist, std::size_t hist_cap, std::size_t* hist_len,
+                      std::size_t* its, std::size_t* mv, int* converged, char* status, double* rho,
+                      double* wall, double* lambda_tilde, double* tuned_lmin) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  return guarded([&] {
+    CaseConfig cfg;
+    cfg.Lx = Lx;
+    cfg.n = n;
+    cfg.factor = factor;
+    cfg.family = fam(family);
+    cfg.k = k;
+    cfg.cycle = cycle == 0 ? Cycle::full : Cycle::one_sided;
+    cfg.driver = driver == 0 ? Driver::pcg : (driver == 1 ? Driver::pgmres : Driver::mg_solver);
+    cfg.tol = tol;
+    cfg.restart = restart;
+    cfg.maxit = maxit;
+    const CaseResult r = run_case_with(cfg, *h);
+    fill_report(r.report, hist, hist_cap, hist_len, its, mv, converged, status, rho, wall);
+    *lambda_tilde = r.lambda_tilde;
+    *tuned_lmin = r.tuned_lambda_min ? *r.tuned_lambda_min : -1.0;
+  });
+}
+
+double ref_estimate_C(void* hp, std::size_t m, std::uint64_t seed) {
+  auto* h = static_cast<Hierarchy*>(hp);
+  return estimate_C(*h, m, seed).C;
+}
+
+// ---- SEM: reference templates driving the oracle's restated SEM operator ----
+
+// Chebyshev-Jacobi smoothing sweep on one SEM level through the reference's
+// chebyshev_smooth (smoothers.hpp:156-172).
+int ref_sem_smooth(void* pmg, int level, int family, std::size_t order, double lmax_mult,
+                   double lmin_mult, const double* b, double* x, int x_is_zero, std::size_t* apps) {
+  auto* p = static_cast<orc_pmg*>(pmg);
+  return guarded([&] {
+    orc_sem* s = orc_pmg_sem(p, level);
+    SemOperator A(orc_pmg_op(p, level), s);
+    const Vec inv_diag = jacobi_inverse_diagonal(A.diagonal());
+    ChebyshevConfig cfg;
+    cfg.family = fam(family);
+    cfg.lambda_tilde = orc_pmg_lambda_tilde(p, level);
+    cfg.lambda_max_multiplier = lmax_mult;
+    cfg.lambda_min_multiplier = lmin_mult;
+    const std::size_t n = A.rows();
+    Vec bv(b, b + n), xv(x, x + n);
+    const std::size_t a0 = A.applications();
+    chebyshev_smooth(A, inv_diag, cfg, order, bv, xv, x_is_zero != 0);
+    *apps = A.applications() - a0;
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+// p-MG preconditioned PGMRES / PCG through the reference's Krylov templates
+// (krylov.hpp:75-264); the preconditioner is the restated multilevel V-cycle.
+int ref_sem_solve(void* pmg, int driver, int family, double lmax_mult, double lmin_mult,
+                  std::size_t k_pre, std::size_t k_post, const double* b, double tol,
+                  std::size_t maxit, std::size_t restart, double* x_out, double* hist,
+                  std::size_t hist_cap, std::size_t* hist_len, std::size_t* its, std::size_t* mv,
+                  int* converged, char* status, double* rho, double* wall) {
+  auto* p = static_cast<orc_pmg*>(pmg);
+  return guarded([&] {
+    SemOperator A(orc_pmg_op(p, 0), orc_pmg_sem(p, 0));
+    const std::size_t n = A.rows();
+    const Preconditioner M = [&](const Vec& v) {
+      Vec z(n, 0.0);
+      if (orc_pmg_v_cycle(p, family, lmax_mult, lmin_mult, k_pre, k_post, v.data(), z.data(), 1))
+        throw std::invalid_argument("pmg v-cycle: invalid smoother configuration");
+      return z;
+    };
+    const Vec bv(b, b + n), x0(n, 0.0);
+    SolveOptions o;
+    o.tol = tol;
+    o.maxit = maxit;
+    o.restart = restart;
+    std::pair<Vec, SolveReport> res =
+        driver == 0 ? pcg(A, M, bv, x0, o) : pgmres(A, M, bv, x0, o);
+    std::memcpy(x_out, res.first.data(), n * sizeof(double));
+    fill_report(res.second, hist, hist_cap, hist_len, its, mv, converged, status, rho, wall);
+  });
+}
+
+}  // extern "C"
