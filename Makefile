@@ -32,7 +32,7 @@ $(OBJ)/k_blas.o $(OBJ)/k_fd.o: $(OBJ)/%.o: $(SRC)/%.cu $(HDR)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) --fmad=false -c $< -o $@
 
-$(OBJ)/k_sem%.o: $(SRC)/k_sem%.cu $(HDR)
+$(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_FAST)): $(OBJ)/%.o: $(SRC)/%.cu $(HDR)
 	@mkdir -p $(OBJ)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

@@ -194,6 +194,10 @@ double orc_pmg_lambda_tilde(const orc_pmg* p, int level);
 int orc_pmg_v_cycle(orc_pmg* p, int family, double lmax_mult, double lmin_mult, size_t k_pre,
                     size_t k_post, const double* b, double* x, int x_is_zero);
 void orc_pmg_coarse_solve(orc_pmg* p, const double* rc, double* ec);
+void orc_pmg_solve(orc_pmg* p, int driver, int family, double lmaxm, double lminm, size_t kpre,
+                   size_t kpost, const double* b, double tol, size_t maxit, size_t restart,
+                   double* x, double* hist, orc_solve_report* rep);
+void orc_kershaw_map(double eps, double x, double y, double z, double* X, double* Y, double* Z);
 
 #ifdef __cplusplus
 }

@@ -680,3 +680,32 @@ int orc_pmg_v_cycle(orc_pmg* p, int family, double lmax_mult, double lmin_mult, 
   orc_cheb_config base = {family, 1.0, lmax_mult, lmin_mult};
   return vcycle_level(p, 0, &base, k_pre, k_post, b, x, x_is_zero);
 }
+
+typedef struct {
+  orc_pmg* p;
+  int family;
+  double lmaxm, lminm;
+  size_t kpre, kpost;
+} pmg_prec_ctx;
+
+static void pmg_prec(void* vctx, const double* v, double* z) { /* multigrid.hpp:94-98 */
+  pmg_prec_ctx* c = vctx;
+  memset(z, 0, c->p->lev[0]->n * sizeof(double));
+  orc_pmg_v_cycle(c->p, c->family, c->lmaxm, c->lminm, c->kpre, c->kpost, v, z, 1);
+}
+
+/* p-MG preconditioned PCG (driver 0) / PGMRES (driver 1) with the restated
+ * reference Krylov drivers (krylov.hpp:75-264); x0 = 0 */
+void orc_pmg_solve(orc_pmg* p, int driver, int family, double lmaxm, double lminm, size_t kpre,
+                   size_t kpost, const double* b, double tol, size_t maxit, size_t restart,
+                   double* x, double* hist, orc_solve_report* rep) {
+  pmg_prec_ctx c = {p, family, lmaxm, lminm, kpre, kpost};
+  const size_t n = p->lev[0]->n;
+  double* x0 = calloc(n, sizeof(double));
+  orc_solve_options o = {tol, maxit, restart, 1};
+  if (driver == 0)
+    orc_pcg(&p->lev[0]->op.base, pmg_prec, &c, b, x0, &o, x, hist, rep);
+  else
+    orc_pgmres(&p->lev[0]->op.base, pmg_prec, &c, b, x0, &o, x, hist, rep);
+  free(x0);
+}

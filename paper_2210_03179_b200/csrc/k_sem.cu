@@ -1,0 +1,738 @@
+// k_sem.cu -- spectral-element kernels for sm_100a (fp64).
+//
+// Hot path: the Chebyshev-Jacobi step on a p-level, i.e. the matrix-free
+// operator A = Q^T A_L Q (sum-factorised tensor contractions with six
+// geometric factors per node) fused with the direct
+// stiffness summation and the three-term recurrence (smoothers.hpp:126-148
+// with S = invD).  One element per (N+1)^2-thread group, one thread per
+// (i,j) column looping over k; the element's u, w_r, w_s live in shared
+// memory, u and w_t columns in registers.  See sem_kernels.hpp for the
+// K1/K2 split that makes QQ^T deterministic and partition-independent.
+#include "sem_kernels.hpp"
+
+namespace cmg {
+
+namespace {
+
+template <int N>
+struct SemC {
+  static constexpr int N1 = N + 1;
+  static constexpr int NP = N1 * N1 * N1;
+  static constexpr int NO = N * N * N;
+  static constexpr int TPE = N1 * N1;  // threads per element
+  static constexpr int EPB = (128 / TPE) > 0 ? (128 / TPE) : 1;  // elements per block
+  static constexpr int NT = EPB * TPE;
+};
+
+// ---------------------------------------------------------------- epilogue
+template <int EPI>
+__device__ __forceinline__ void epilogue(const SemArgs& A, long slot, double w, double dv) {
+  if constexpr (EPI == EPI_STORE) {
+    A.y[slot] = w;
+  } else if constexpr (EPI == EPI_ADD) {
+    A.y[slot] += w;
+  } else if constexpr (EPI == EPI_RESID) {
+    A.r[slot] = A.b[slot] - w;
+  } else if constexpr (EPI == EPI_CHEB4) {
+    // smoothers.hpp:138-144: x += beta d ; r -= A d ; d = c1 d + c2 invD r
+    A.x[slot] = A.x_zero ? A.beta * dv : A.x[slot] + A.beta * dv;
+    const double rv = A.r_in[slot] - w;
+    A.r[slot] = rv;
+    A.d_out[slot] = A.c1 * dv + A.c2 * A.invd[slot] * rv;
+  } else if constexpr (EPI == EPI_CHEB1) {
+    // smoothers.hpp:109-118: x += d ; z -= invD A d ; d = c1 d + c2 z
+    A.x[slot] = A.x_zero ? dv : A.x[slot] + dv;
+    const double zv = A.r[slot] - A.invd[slot] * w;
+    A.r[slot] = zv;
+    A.d_out[slot] = A.c1 * dv + A.c2 * zv;
+  } else if constexpr (EPI == EPI_CHEB4_INIT) {
+    const double rv = A.b[slot] - w;
+    A.r[slot] = rv;
+    A.d_out[slot] = A.c0 * A.invd[slot] * rv;
+  } else if constexpr (EPI == EPI_CHEB1_INIT) {
+    const double zv = (A.b[slot] - w) * A.invd[slot];
+    A.r[slot] = zv;
+    A.d_out[slot] = zv / A.theta;
+  }
+}
+
+// owner slot of local node index `l` (0..N) along one dimension for element coordinate `ec`:
+// returns owner element coordinate and in-element slot coordinate; -1 if Dirichlet.
+template <int N>
+__device__ __forceinline__ int owner1d(int ec, int l, int ne, int& oe) {
+  // global index g = ec*N + l ; interior iff 0 < g < N*ne
+  const int g = ec * N + l;
+  if (g <= 0 || g >= N * ne) return -1;
+  oe = (g - 1) / N;
+  return (g - 1) - oe * N;
+}
+
+// ---------------------------------------------------------------- K1
+template <int N, int MODE, int EPI>
+__global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1(SemArgs A) {
+  using C = SemC<N>;
+  constexpr int N1 = C::N1, NP = C::NP, NO = C::NO, TPE = C::TPE, EPB = C::EPB;
+  __shared__ double sD[N1][N1 + 1];
+  __shared__ double su[EPB][NP];
+  __shared__ double sr[EPB][NP];
+  __shared__ double ss[EPB][NP];
+  const int le = threadIdx.x / TPE;
+  const int t = threadIdx.x - le * TPE;
+  const int i = t % N1, j = t / N1;
+  const long e = A.e_begin + (long)blockIdx.x * EPB + le;
+  const bool active = e < A.e_end;
+  for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) sD[q / N1][q % N1] = A.D[q];
+  const int ex = active ? (int)(e % A.Ex) : 0;
+  const int ey = active ? (int)((e / A.Ex) % A.Ey) : 0;
+  const int ez = active ? (int)(e / ((long)A.Ex * A.Ey)) : 0;
+  double u[N1];
+  if constexpr (MODE == SEM_AX) {
+    // gather Q u: local (i,j,k) -> owner slot (or halo / Dirichlet zero)
+    int oex, oey;
+    const int ax = owner1d<N>(ex, i, A.Ex, oex);
+    const int ay = owner1d<N>(ey, j, A.Ey, oey);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      double v = 0.0;
+      if (active && ax >= 0 && ay >= 0) {
+        int oez;
+        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
+        if (az >= 0) {
+          const int lz = oez - A.z0;
+          if (lz < 0) {
+            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
+          } else {
+            const long oe = (long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz);
+            v = A.u[oe * NO + ax + N * (ay + N * az)];
+          }
+        }
+      }
+      u[k] = v;
+      su[le][(k * N1 + j) * N1 + i] = v;
+    }
+  }
+  __syncthreads();
+  double out[N1];
+  if constexpr (MODE == SEM_AX) {
+    const double* Ge = A.G + (active ? e : 0) * 6 * NP;
+    double wt[N1];
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int l = (k * N1 + j) * N1 + i;
+      double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        ur += sD[i][m] * su[le][(k * N1 + j) * N1 + m];
+        us += sD[j][m] * su[le][(k * N1 + m) * N1 + i];
+        ut += sD[k][m] * u[m];
+      }
+      double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
+      if (active) {
+        g0 = __ldg(Ge + l);
+        g1 = __ldg(Ge + NP + l);
+        g2 = __ldg(Ge + 2 * NP + l);
+        g3 = __ldg(Ge + 3 * NP + l);
+        g4 = __ldg(Ge + 4 * NP + l);
+        g5 = __ldg(Ge + 5 * NP + l);
+      }
+      sr[le][l] = g0 * ur + g1 * us + g2 * ut;
+      ss[le][l] = g1 * ur + g3 * us + g4 * ut;
+      wt[k] = g2 * ur + g4 * us + g5 * ut;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        v += sD[m][i] * sr[le][(k * N1 + j) * N1 + m];
+        v += sD[m][j] * ss[le][(k * N1 + m) * N1 + i];
+        v += sD[m][k] * wt[m];
+      }
+      out[k] = v;
+    }
+  } else {
+    const double* Le = A.lvec + (active ? e : 0) * NP;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) out[k] = active ? Le[(k * N1 + j) * N1 + i] : 0.0;
+  }
+  if (!active) return;
+  // epilogue: interior nodes finished here, shell nodes to the shell buffer
+  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    if (ij_interior && k >= 1 && k < N) {
+      const long slot = e * NO + (i - 1) + N * ((j - 1) + N * (k - 1));
+      double dv = 0.0;
+      if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) dv = u[k];
+      epilogue<EPI>(A, slot, out[k], dv);
+    } else {
+      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = out[k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K2
+template <int N, int EPI>
+__global__ void k_sem_k2(SemArgs A) {
+  constexpr int N1 = N + 1, NO = N * N * N;
+  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long q = tid / A.nshared;
+  const int s = (int)(tid - q * A.nshared);
+  const long e = A.e_begin + q;
+  if (e >= A.e_end) return;
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  const int sl = A.shared[s];
+  const int a = sl % N, b = (sl / N) % N, c = sl / (N * N);
+  // padding (far domain boundary) is not an unknown
+  if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
+  const int i = a + 1, j = b + 1, k = c + 1;
+  const int nz = (k == N) ? 2 : 1, ny = (j == N) ? 2 : 1, nx = (i == N) ? 2 : 1;
+  double sum = 0.0;
+  for (int dz = 0; dz < nz; ++dz)
+    for (int dy = 0; dy < ny; ++dy)
+      for (int dx = 0; dx < nx; ++dx) {
+        const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
+        double v;
+        if (ez + dz >= A.Ezl) {
+          v = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + li + N1 * lj];
+        } else {
+          const long e2 = e + dx + (long)A.Ex * (dy + (long)A.Ey * dz);
+          v = A.shell[e2 * A.nshell + A.lut[(lk * N1 + lj) * N1 + li]];
+        }
+        sum += v;
+      }
+  const long slot = e * NO + sl;
+  double dv = 0.0;
+  if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) dv = A.d[slot];
+  epilogue<EPI>(A, slot, sum, dv);
+}
+
+template <int N, int MODE, int EPI>
+void launch_k1(const SemArgs& a, cudaStream_t s) {
+  using C = SemC<N>;
+  const long ne = a.e_end - a.e_begin;
+  if (ne <= 0) return;
+  const long blocks = (ne + C::EPB - 1) / C::EPB;
+  k_sem_k1<N, MODE, EPI><<<(unsigned)blocks, C::NT, 0, s>>>(a);
+  CMG_LAUNCH_CHECK();
+}
+
+template <int N, int EPI>
+void launch_k2(const SemArgs& a, cudaStream_t s) {
+  const long ne = a.e_end - a.e_begin;
+  if (ne <= 0 || a.nshared == 0) return;
+  const long threads = ne * a.nshared;
+  k_sem_k2<N, EPI><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+  CMG_LAUNCH_CHECK();
+}
+
+template <int N, int MODE>
+void dispatch_k1_epi(const SemArgs& a, int epi, cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE: return launch_k1<N, MODE, EPI_STORE>(a, s);
+    case EPI_ADD: return launch_k1<N, MODE, EPI_ADD>(a, s);
+    case EPI_RESID: return launch_k1<N, MODE, EPI_RESID>(a, s);
+    case EPI_CHEB4: return launch_k1<N, MODE, EPI_CHEB4>(a, s);
+    case EPI_CHEB1: return launch_k1<N, MODE, EPI_CHEB1>(a, s);
+    case EPI_CHEB4_INIT: return launch_k1<N, MODE, EPI_CHEB4_INIT>(a, s);
+    case EPI_CHEB1_INIT: return launch_k1<N, MODE, EPI_CHEB1_INIT>(a, s);
+  }
+  throw Error(EINVAL_, "sem_k1: bad epilogue");
+}
+
+template <int N>
+void dispatch_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
+  if (mode == SEM_AX) dispatch_k1_epi<N, SEM_AX>(a, epi, s);
+  else dispatch_k1_epi<N, SEM_LVEC>(a, epi, s);
+}
+
+template <int N>
+void dispatch_k2(const SemArgs& a, int epi, cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE: return launch_k2<N, EPI_STORE>(a, s);
+    case EPI_ADD: return launch_k2<N, EPI_ADD>(a, s);
+    case EPI_RESID: return launch_k2<N, EPI_RESID>(a, s);
+    case EPI_CHEB4: return launch_k2<N, EPI_CHEB4>(a, s);
+    case EPI_CHEB1: return launch_k2<N, EPI_CHEB1>(a, s);
+    case EPI_CHEB4_INIT: return launch_k2<N, EPI_CHEB4_INIT>(a, s);
+    case EPI_CHEB1_INIT: return launch_k2<N, EPI_CHEB1_INIT>(a, s);
+  }
+  throw Error(EINVAL_, "sem_k2: bad epilogue");
+}
+
+// ---------------------------------------------------------------- pointwise
+__global__ void k_cheb4_init_zero(std::size_t n, const double* __restrict__ b,
+                                  const double* __restrict__ invd, double c0, double* __restrict__ r,
+                                  double* __restrict__ d) {
+  for (std::size_t q = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; q < n;
+       q += (std::size_t)gridDim.x * blockDim.x) {
+    const double rv = b[q];
+    r[q] = rv;
+    d[q] = c0 * invd[q] * rv;
+  }
+}
+
+__global__ void k_cheb1_init_zero(std::size_t n, const double* __restrict__ b,
+                                  const double* __restrict__ invd, double theta,
+                                  double* __restrict__ z, double* __restrict__ d) {
+  for (std::size_t q = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; q < n;
+       q += (std::size_t)gridDim.x * blockDim.x) {
+    const double zv = b[q] * invd[q];
+    z[q] = zv;
+    d[q] = zv / theta;
+  }
+}
+
+inline unsigned vgrid(std::size_t n) {
+  std::size_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+// ---------------------------------------------------------------- halo packing
+__global__ void k_pack_top(SemArgs A, const double* __restrict__ u, double* __restrict__ buf) {
+  const int N = A.N;
+  const long n = (long)A.Ex * A.Ey * N * N;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int ab = (int)(t % (N * N));
+  const long exy = t / (N * N);
+  const long e = exy + (long)A.Ex * A.Ey * (A.Ezl - 1);
+  buf[t] = u[e * N * N * N + ab + (long)N * N * (N - 1)];
+}
+
+__global__ void k_pack_contrib_bottom(SemArgs A, double* __restrict__ buf) {
+  const int N1 = A.N + 1;
+  const long n = (long)A.Ex * A.Ey * N1 * N1;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int ij = (int)(t % (N1 * N1));
+  const long e = t / (N1 * N1);  // layer 0
+  buf[t] = A.shell[e * A.nshell + A.lut[ij]];  // k = 0 plane: lut index (0*N1 + j)*N1 + i = ij
+}
+
+// ---------------------------------------------------------------- geometry (setup)
+__device__ double kr_right(double eps, double x) { return (x <= 0.5) ? (2.0 - eps) * x : 1.0 + eps * (x - 1.0); }
+__device__ double kr_left(double eps, double x) { return 1.0 - kr_right(eps, 1.0 - x); }
+__device__ double kr_step(double a, double b, double x) {
+  if (x <= 0.0) return a;
+  if (x >= 1.0) return b;
+  return a + (b - a) * (x * x * x * (x * (6.0 * x - 15.0) + 10.0));
+}
+
+// Kershaw map (same definition as oracle/oracle_sem.c)
+__device__ void kershaw(double eps, double x, double y, double z, double& X, double& Y, double& Z) {
+  X = x;
+  int layer = (int)(x * 6.0);
+  if (layer > 5) layer = 5;
+  const double lam = (x - layer / 6.0) * 6.0;
+  switch (layer) {
+    case 0: Y = kr_left(eps, y); Z = kr_left(eps, z); break;
+    case 1:
+    case 4:
+      Y = kr_step(kr_left(eps, y), kr_right(eps, y), lam);
+      Z = kr_step(kr_left(eps, z), kr_right(eps, z), lam);
+      break;
+    case 2:
+      Y = kr_step(kr_right(eps, y), kr_left(eps, y), lam / 2.0);
+      Z = kr_step(kr_right(eps, z), kr_left(eps, z), lam / 2.0);
+      break;
+    case 3:
+      Y = kr_step(kr_right(eps, y), kr_left(eps, y), (1.0 + lam) / 2.0);
+      Z = kr_step(kr_right(eps, z), kr_left(eps, z), (1.0 + lam) / 2.0);
+      break;
+    default: Y = kr_right(eps, y); Z = kr_right(eps, z); break;
+  }
+}
+
+// one block per element, one thread per node
+__global__ void k_geometry(SemGeom g, double* __restrict__ G, double* __restrict__ Lrhs,
+                           double* __restrict__ Lmass) {
+  extern __shared__ double sm[];
+  const int N = g.N, N1 = N + 1, NP = N1 * N1 * N1;
+  double* X = sm;
+  double* Y = sm + NP;
+  double* Z = sm + 2 * NP;
+  const long e = blockIdx.x;
+  const int ex = (int)(e % g.Ex), ey = (int)((e / g.Ex) % g.Ey), ez = g.z0 + (int)(e / ((long)g.Ex * g.Ey));
+  for (int l = threadIdx.x; l < NP; l += blockDim.x) {
+    const int i = l % N1, j = (l / N1) % N1, k = l / (N1 * N1);
+    const double x = ((double)ex + 0.5 * (g.xi[i] + 1.0)) / (double)g.Ex;
+    const double y = ((double)ey + 0.5 * (g.xi[j] + 1.0)) / (double)g.Ey;
+    const double z = ((double)ez + 0.5 * (g.xi[k] + 1.0)) / (double)g.Ez;
+    double u = x, v = y, w = z;
+    if (g.geometry == 1) kershaw(g.eps, x, y, z, u, v, w);
+    X[l] = u - 0.5;
+    Y[l] = v - 0.5;
+    Z[l] = w - 0.5;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < NP; l += blockDim.x) {
+    const int i = l % N1, j = (l / N1) % N1, k = l / (N1 * N1);
+    double Jm[3][3];
+    const double* Cc[3] = {X, Y, Z};
+    for (int c = 0; c < 3; ++c) {
+      double dr = 0, ds = 0, dt = 0;
+      for (int m = 0; m < N1; ++m) {
+        dr += g.D[i * N1 + m] * Cc[c][m + N1 * (j + N1 * k)];
+        ds += g.D[j * N1 + m] * Cc[c][i + N1 * (m + N1 * k)];
+        dt += g.D[k * N1 + m] * Cc[c][i + N1 * (j + N1 * m)];
+      }
+      Jm[c][0] = dr; Jm[c][1] = ds; Jm[c][2] = dt;
+    }
+    const double det = Jm[0][0] * (Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1]) -
+                       Jm[0][1] * (Jm[1][0] * Jm[2][2] - Jm[1][2] * Jm[2][0]) +
+                       Jm[0][2] * (Jm[1][0] * Jm[2][1] - Jm[1][1] * Jm[2][0]);
+    double Ji[3][3];
+    Ji[0][0] = (Jm[1][1] * Jm[2][2] - Jm[1][2] * Jm[2][1]) / det;
+    Ji[0][1] = (Jm[0][2] * Jm[2][1] - Jm[0][1] * Jm[2][2]) / det;
+    Ji[0][2] = (Jm[0][1] * Jm[1][2] - Jm[0][2] * Jm[1][1]) / det;
+    Ji[1][0] = (Jm[1][2] * Jm[2][0] - Jm[1][0] * Jm[2][2]) / det;
+    Ji[1][1] = (Jm[0][0] * Jm[2][2] - Jm[0][2] * Jm[2][0]) / det;
+    Ji[1][2] = (Jm[0][2] * Jm[1][0] - Jm[0][0] * Jm[1][2]) / det;
+    Ji[2][0] = (Jm[1][0] * Jm[2][1] - Jm[1][1] * Jm[2][0]) / det;
+    Ji[2][1] = (Jm[0][1] * Jm[2][0] - Jm[0][0] * Jm[2][1]) / det;
+    Ji[2][2] = (Jm[0][0] * Jm[1][1] - Jm[0][1] * Jm[1][0]) / det;
+    const double W = g.w[i] * g.w[j] * g.w[k] * det;
+    const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {0, 1, 2, 1, 2, 2};
+    for (int q = 0; q < 6; ++q) {
+      const int a = pa[q], b = pb[q];
+      G[(e * 6 + q) * NP + l] = W * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+    }
+    if (Lmass) Lmass[e * NP + l] = W;
+    if (Lrhs) {
+      const double pi = 3.141592653589793238462643383279502884;
+      const double f = 3.0 * pi * pi * sin(pi * X[l]) * sin(pi * Y[l]) * sin(pi * Z[l]);
+      Lrhs[e * NP + l] = W * f;
+    }
+  }
+}
+
+// App. A5 diagonal, one block per element
+__global__ void k_local_diag(int N, const double* __restrict__ G, const double* __restrict__ D,
+                             double* __restrict__ Ld) {
+  const int N1 = N + 1, NP = N1 * N1 * N1;
+  const long e = blockIdx.x;
+  const double* Ge = G + e * 6 * NP;
+  for (int l = threadIdx.x; l < NP; l += blockDim.x) {
+    const int i = l % N1, j = (l / N1) % N1, k = l / (N1 * N1);
+    double v = 0;
+    for (int m = 0; m < N1; ++m) {
+      v += D[m * N1 + i] * D[m * N1 + i] * Ge[m + N1 * (j + N1 * k)];
+      v += D[m * N1 + j] * D[m * N1 + j] * Ge[3 * NP + i + N1 * (m + N1 * k)];
+      v += D[m * N1 + k] * D[m * N1 + k] * Ge[5 * NP + i + N1 * (j + N1 * m)];
+    }
+    v += 2.0 * D[i * N1 + i] * D[j * N1 + j] * Ge[NP + l];
+    v += 2.0 * D[i * N1 + i] * D[k * N1 + k] * Ge[2 * NP + l];
+    v += 2.0 * D[j * N1 + j] * D[k * N1 + k] * Ge[4 * NP + l];
+    Ld[e * NP + l] = v;
+  }
+}
+
+__device__ __forceinline__ bool slot_valid(const SemArgs& A, long q) {
+  const int N = A.N;
+  const long NO = (long)N * N * N;
+  const long e = q / NO;
+  const int sl = (int)(q - e * NO);
+  const int a = sl % N, b = (sl / N) % N, c = sl / (N * N);
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  return ex * N + a + 1 < N * A.Ex && ey * N + b + 1 < N * A.Ey && (A.z0 + ez) * N + c + 1 < N * A.Ez;
+}
+
+__global__ void k_inverse_diag(SemArgs A, const double* __restrict__ d, double* __restrict__ inv,
+                               int* zero_flag) {
+  const long n = A.E * (long)A.N * A.N * A.N;
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) {
+    if (slot_valid(A, q)) {
+      const double v = d[q];
+      if (v == 0.0) atomicExch(zero_flag, 1);
+      inv[q] = 1.0 / v;
+    } else {
+      inv[q] = 0.0;
+    }
+  }
+}
+
+__global__ void k_slot_mask(SemArgs A, double* __restrict__ m) {
+  const long n = A.E * (long)A.N * A.N * A.N;
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x)
+    m[q] = slot_valid(A, q) ? 1.0 : 0.0;
+}
+
+// ---------------------------------------------------------------- p-transfers
+// one block per fine element; smem staging of the coarse element values
+template <int NF, int NCO>
+__global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
+                          const double* __restrict__ xc, double* __restrict__ yf, int add) {
+  constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF, NOC = NCO * NCO * NCO;
+  __shared__ double sJ[F1 * C1];
+  __shared__ double uc[C1 * C1 * C1];
+  __shared__ double t1[F1 * C1 * C1];
+  __shared__ double t2[F1 * F1 * C1];
+  const long e = blockIdx.x;
+  const int ex = (int)(e % F.Ex), ey = (int)((e / F.Ex) % F.Ey), ez = (int)(e / ((long)F.Ex * F.Ey));
+  for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
+  for (int q = threadIdx.x; q < C1 * C1 * C1; q += blockDim.x) {
+    const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
+    int oex, oey, oez;
+    const int ax = owner1d<NCO>(ex, a, Cc.Ex, oex);
+    const int ay = owner1d<NCO>(ey, b, Cc.Ey, oey);
+    const int az = owner1d<NCO>(Cc.z0 + ez, c, Cc.Ez, oez);
+    double v = 0.0;
+    if (ax >= 0 && ay >= 0 && az >= 0) {
+      const int lz = oez - Cc.z0;
+      if (lz < 0)
+        v = Cc.halo_lo[((long)oex + (long)Cc.Ex * oey) * (NCO * NCO) + ax + NCO * ay];
+      else
+        v = xc[((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOC + ax + NCO * (ay + NCO * az)];
+    }
+    uc[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < F1 * C1 * C1; q += blockDim.x) {  // contract x
+    const int i = q % F1, b = (q / F1) % C1, c = q / (F1 * C1);
+    double v = 0.0;
+    for (int m = 0; m < C1; ++m) v += sJ[i * C1 + m] * uc[m + C1 * (b + C1 * c)];
+    t1[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < F1 * F1 * C1; q += blockDim.x) {  // contract y
+    const int i = q % F1, j = (q / F1) % F1, c = q / (F1 * F1);
+    double v = 0.0;
+    for (int m = 0; m < C1; ++m) v += sJ[j * C1 + m] * t1[i + F1 * (m + C1 * c)];
+    t2[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NOF; q += blockDim.x) {  // contract z at owned fine nodes
+    const int a = q % NF, b = (q / NF) % NF, c = q / (NF * NF);
+    const int i = a + 1, j = b + 1, k = c + 1;
+    if (ex * NF + i >= NF * F.Ex || ey * NF + j >= NF * F.Ey || (F.z0 + ez) * NF + k >= NF * F.Ez) continue;
+    double v = 0.0;
+    for (int m = 0; m < C1; ++m) v += sJ[k * C1 + m] * t2[i + F1 * (j + F1 * m)];
+    const long slot = e * NOF + q;
+    yf[slot] = add ? yf[slot] + v : v;
+  }
+}
+
+template <int NF, int NCO>
+__global__ void k_restrict_local(SemArgs F, const double* __restrict__ J, const double* __restrict__ xf,
+                                 double* __restrict__ Lc) {
+  constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF, CP = C1 * C1 * C1;
+  __shared__ double sJ[F1 * C1];
+  __shared__ double uf[F1 * F1 * F1];
+  __shared__ double t1[C1 * F1 * F1];
+  __shared__ double t2[C1 * C1 * F1];
+  const long e = blockIdx.x;
+  for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
+  for (int q = threadIdx.x; q < F1 * F1 * F1; q += blockDim.x) {
+    const int i = q % F1, j = (q / F1) % F1, k = q / (F1 * F1);
+    double v = 0.0;
+    if (i >= 1 && j >= 1 && k >= 1) v = xf[e * NOF + (i - 1) + NF * ((j - 1) + NF * (k - 1))];
+    uf[q] = v;  // padding slots are zero
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < C1 * F1 * F1; q += blockDim.x) {  // J^T along x
+    const int a = q % C1, j = (q / C1) % F1, k = q / (C1 * F1);
+    double v = 0.0;
+    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + a] * uf[m + F1 * (j + F1 * k)];
+    t1[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < C1 * C1 * F1; q += blockDim.x) {
+    const int a = q % C1, b = (q / C1) % C1, k = q / (C1 * C1);
+    double v = 0.0;
+    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + b] * t1[a + C1 * (m + F1 * k)];
+    t2[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < CP; q += blockDim.x) {
+    const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
+    double v = 0.0;
+    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + c] * t2[a + C1 * (b + C1 * m)];
+    Lc[e * CP + q] = v;
+  }
+}
+
+// ---------------------------------------------------------------- layer dots
+// partials[(v*L + layer)*CH + chunk]
+constexpr int LCH = 16;
+__global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int nv,
+                             const double* __restrict__ w, long layer_len, int nlayers,
+                             double* __restrict__ partials) {
+  const int layer = blockIdx.y, chunk = blockIdx.x, v0 = blockIdx.z * 8;
+  const int cnt = min(8, nv - v0);
+  __shared__ double sh[8][8];
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  const long base = (long)layer * layer_len;
+  for (long q = (long)chunk * blockDim.x + threadIdx.x; q < layer_len; q += (long)LCH * blockDim.x) {
+    const double wv = w[base + q];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < cnt) acc[c] += V[(std::size_t)(v0 + c) * ldv + base + q] * wv;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[c][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < cnt) {
+    double s = 0.0;
+    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) s += sh[threadIdx.x][wv];
+    partials[((long)(v0 + threadIdx.x) * nlayers + layer) * LCH + chunk] = s;
+  }
+}
+
+__global__ void k_layer_reduce(const double* __restrict__ partials, int nv, int nlayers,
+                               double* __restrict__ out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)nv * nlayers) return;
+  double s = 0.0;
+  for (int c = 0; c < LCH; ++c) s += partials[t * LCH + c];
+  out[t] = s;  // out[v*nlayers + layer]
+}
+
+__global__ void k_layer_finalize(const double* __restrict__ g, int nv, const int* __restrict__ lpr,
+                                 int nranks, double* __restrict__ out, int do_sqrt) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double s = 0.0;
+  long off = 0;
+  for (int r = 0; r < nranks; ++r) {
+    const int L = lpr[r];
+    for (int l = 0; l < L; ++l) s += g[off + (long)v * L + l];
+    off += (long)nv * L;
+  }
+  out[v] = do_sqrt ? sqrt(s) : s;
+}
+
+}  // namespace
+
+// ====================================================================== host launchers
+void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
+  switch (a.N) {
+    case 1: return dispatch_k1<1>(a, mode, epi, s);
+    case 2: return dispatch_k1<2>(a, mode, epi, s);
+    case 3: return dispatch_k1<3>(a, mode, epi, s);
+    case 4: return dispatch_k1<4>(a, mode, epi, s);
+    case 5: return dispatch_k1<5>(a, mode, epi, s);
+    case 7: return dispatch_k1<7>(a, mode, epi, s);
+  }
+  throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
+}
+
+void sem_k2(const SemArgs& a, int epi, cudaStream_t s) {
+  switch (a.N) {
+    case 1: return dispatch_k2<1>(a, epi, s);
+    case 2: return dispatch_k2<2>(a, epi, s);
+    case 3: return dispatch_k2<3>(a, epi, s);
+    case 4: return dispatch_k2<4>(a, epi, s);
+    case 5: return dispatch_k2<5>(a, epi, s);
+    case 7: return dispatch_k2<7>(a, epi, s);
+  }
+  throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
+}
+
+void sem_cheb4_init_zero(std::size_t n, const double* b, const double* invd, double c0, double* r,
+                         double* d, cudaStream_t s) {
+  k_cheb4_init_zero<<<vgrid(n), 256, 0, s>>>(n, b, invd, c0, r, d);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_cheb1_init_zero(std::size_t n, const double* b, const double* invd, double theta,
+                         double* z, double* d, cudaStream_t s) {
+  k_cheb1_init_zero<<<vgrid(n), 256, 0, s>>>(n, b, invd, theta, z, d);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_pack_top(const SemArgs& a, const double* u, double* buf, cudaStream_t s) {
+  const long n = (long)a.Ex * a.Ey * a.N * a.N;
+  k_pack_top<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, u, buf);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_pack_contrib_bottom(const SemArgs& a, double* buf, cudaStream_t s) {
+  const long n = (long)a.Ex * a.Ey * (a.N + 1) * (a.N + 1);
+  k_pack_contrib_bottom<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, buf);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_geometry(const SemGeom& g, double* G, double* Lrhs, double* Lmass, cudaStream_t s) {
+  const long E = (long)g.Ex * g.Ey * g.Ezl;
+  const int NP = (g.N + 1) * (g.N + 1) * (g.N + 1);
+  k_geometry<<<(unsigned)E, 128, 3 * NP * sizeof(double), s>>>(g, G, Lrhs, Lmass);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_local_diag(int N, long E, const double* G, const double* D, double* Ldiag, cudaStream_t s) {
+  k_local_diag<<<(unsigned)E, 128, 0, s>>>(N, G, D, Ldiag);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_inverse_diag(const SemArgs& a, const double* diag, double* invd, int* zero_flag,
+                      cudaStream_t s) {
+  const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
+  k_inverse_diag<<<vgrid(n), 256, 0, s>>>(a, diag, invd, zero_flag);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_slot_mask(const SemArgs& a, double* mask, cudaStream_t s) {
+  const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
+  k_slot_mask<<<vgrid(n), 256, 0, s>>>(a, mask);
+  CMG_LAUNCH_CHECK();
+}
+
+template <int NF, int NCO>
+static void prolong_t(const SemArgs& f, const SemArgs& c, const double* J, const double* xc, double* yf,
+                      bool add, cudaStream_t s) {
+  k_prolong<NF, NCO><<<(unsigned)f.E, 128, 0, s>>>(f, c, J, xc, yf, add ? 1 : 0);
+  CMG_LAUNCH_CHECK();
+}
+
+template <int NF, int NCO>
+static void restrict_t(const SemArgs& f, const double* J, const double* xf, double* Lc, cudaStream_t s) {
+  k_restrict_local<NF, NCO><<<(unsigned)f.E, 128, 0, s>>>(f, J, xf, Lc);
+  CMG_LAUNCH_CHECK();
+}
+
+#define CMG_PAIRS(X) X(7, 3) X(7, 5) X(5, 3) X(3, 1) X(7, 1) X(5, 1) X(4, 2) X(2, 1) X(3, 2) X(4, 1)
+
+void sem_prolong(const SemArgs& f, const SemArgs& c, const double* J, const double* xc, double* yf,
+                 bool add, cudaStream_t s) {
+#define X(a, b) if (f.N == a && c.N == b) return prolong_t<a, b>(f, c, J, xc, yf, add, s);
+  CMG_PAIRS(X)
+#undef X
+  throw Error(EINVAL_, "unsupported p-multigrid order pair");
+}
+
+void sem_restrict_local(const SemArgs& f, int Nc, const double* J, const double* xf, double* Lc,
+                        cudaStream_t s) {
+#define X(a, b) if (f.N == a && Nc == b) return restrict_t<a, b>(f, J, xf, Lc, s);
+  CMG_PAIRS(X)
+#undef X
+  throw Error(EINVAL_, "unsupported p-multigrid order pair");
+}
+
+void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
+                    int nlayers, double* partials, double* out, cudaStream_t s) {
+  dim3 grid(LCH, nlayers, (nv + 7) / 8);
+  k_layer_dots<<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+  CMG_LAUNCH_CHECK();
+  const long t = (long)nv * nlayers;
+  k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_layer_finalize(const double* gathered, int nv, const int* lpr, int nranks, double* out,
+                        int do_sqrt, cudaStream_t s) {
+  k_layer_finalize<<<(nv + 63) / 64, 64, 0, s>>>(gathered, nv, lpr, nranks, out, do_sqrt);
+  CMG_LAUNCH_CHECK();
+}
+
+}  // namespace cmg

@@ -1,0 +1,679 @@
+// sem.cpp -- host side of the spectral-element p-multigrid path.
+//
+// SemLevel is the LinearOperatorLike for one p-level on one rank's z-slab of
+// elements (operators.hpp:19-26 shape): apply / residual / diagonal and the
+// fused Chebyshev-Jacobi steps all run as K1 + K2 kernel pairs (k_sem.cu),
+// with the NCCL face halo (input top face up, bottom-face contributions down)
+// between them when the mesh is partitioned.  Inner products are reduced per
+// element layer and summed in global z order on every rank, so every result
+// is bitwise identical for 1, 2, 4 or 8 GPUs.
+//
+// Pmg is the p-multigrid hierarchy with the reference's
+// V-cycle control flow (multigrid.hpp:69-90) applied recursively.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cmg_objects.hpp"
+#include "sem_kernels.hpp"
+
+using namespace cmg;
+
+namespace {
+
+[[noreturn]] void fail(int code, const std::string& m) { throw cmg::Error(code, m); }
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return CMG_OK;
+  } catch (const cmg::Error& e) {
+    cmg::set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    cmg::set_last_error(e.what());
+    return CMG_ERUNTIME;
+  }
+}
+
+struct IBuf {
+  int* p = nullptr;
+  void upload(const std::vector<int>& h) {
+    if (p) cudaFree(p);
+    CMG_CUDA(cudaMalloc(&p, std::max<std::size_t>(1, h.size()) * sizeof(int)));
+    if (!h.empty()) CMG_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  ~IBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+void validate_desc(const cmg_sem_desc& d) {
+  if (d.order < 1 || d.order > 7 || d.order == 6)
+    fail(CMG_EINVAL, "sem: order must be one of 1,2,3,4,5,7");
+  if (d.ex < 1 || d.ey < 1 || d.ez < 1) fail(CMG_EINVAL, "sem: element counts must be positive");
+  if (d.nranks < 1 || d.rank < 0 || d.rank >= d.nranks) fail(CMG_EINVAL, "sem: bad rank/nranks");
+  if (d.nranks > d.ez) fail(CMG_EINVAL, "sem: more ranks than element layers");
+  if (d.geometry != 0 && d.geometry != 1) fail(CMG_EINVAL, "sem: geometry must be 0 (box) or 1 (Kershaw)");
+  if (d.geometry == 1 && !(d.eps > 0.0 && d.eps <= 1.0)) fail(CMG_EINVAL, "sem: Kershaw eps must be in (0,1]");
+}
+
+// z-slab partition (contiguous element layers)
+void partition(const cmg_sem_desc& d, int& z0, int& z1) {
+  z0 = static_cast<int>((static_cast<long>(d.rank) * d.ez) / d.nranks);
+  z1 = static_cast<int>((static_cast<long>(d.rank + 1) * d.ez) / d.nranks);
+}
+
+long canonical_of_slot(const cmg_sem_desc& d, int z0, long q) {
+  const int N = d.order;
+  const long NO = static_cast<long>(N) * N * N;
+  const long e = q / NO;
+  const int sl = static_cast<int>(q - e * NO);
+  const int a = sl % N, b = (sl / N) % N, c = sl / (N * N);
+  const int ex = static_cast<int>(e % d.ex), ey = static_cast<int>((e / d.ex) % d.ey);
+  const int ez = z0 + static_cast<int>(e / (static_cast<long>(d.ex) * d.ey));
+  const long gx = static_cast<long>(ex) * N + a + 1, gy = static_cast<long>(ey) * N + b + 1,
+             gz = static_cast<long>(ez) * N + c + 1;
+  const long Mx = static_cast<long>(N) * d.ex - 1, My = static_cast<long>(N) * d.ey - 1,
+             Mz = static_cast<long>(N) * d.ez - 1;
+  if (gx > Mx || gy > My || gz > Mz) return -1;
+  return ((gz - 1) * My + (gy - 1)) * Mx + (gx - 1);
+}
+
+}  // namespace
+
+// ============================================================== SemLevel
+struct SemLevel final : cmg_op {
+  cmg_sem_desc desc{};
+  int N = 7, Ex = 1, Ey = 1, Ez = 1, z0 = 0, z1 = 1, Ezl = 1;
+  long E = 0;
+  int nshell = 0, nshared = 0;
+  DBuf G, Dm, xi, w, shell, halo_lo, halo_send, contrib_hi, contrib_send, diagv, mask, Lrhs;
+  DBuf lpart, lout, lgath;
+  IBuf lut, shared, lpr;
+  std::vector<int> lpr_h;
+
+  SemLevel(cmg_ctx* c, const cmg_sem_desc& d) {
+    validate_desc(d);
+    ctx = c;
+    desc = d;
+    N = d.order;
+    Ex = d.ex;
+    Ey = d.ey;
+    Ez = d.ez;
+    partition(d, z0, z1);
+    Ezl = z1 - z0;
+    if (d.nranks > 1) {
+      if (d.ez % d.nranks != 0) fail(CMG_EINVAL, "sem: ez must be divisible by nranks");
+      if (!ctx->comm || ctx->nranks != d.nranks || ctx->rank != d.rank)
+        fail(CMG_EINVAL, "sem: context has no matching NCCL communicator (cmg_ctx_attach_nccl)");
+    }
+    E = static_cast<long>(Ex) * Ey * Ezl;
+    const long NO = static_cast<long>(N) * N * N;
+    len = static_cast<std::size_t>(E * NO);
+    n = static_cast<std::size_t>((static_cast<long>(N) * Ex - 1) * (static_cast<long>(N) * Ey - 1) *
+                                 (static_cast<long>(N) * Ez - 1));
+    const int N1 = N + 1, NP = N1 * N1 * N1;
+    // shell LUT and shared-owned list
+    std::vector<int> lut_h(NP, -1), sh_h;
+    nshell = 0;
+    for (int k = 0; k < N1; ++k)
+      for (int j = 0; j < N1; ++j)
+        for (int i = 0; i < N1; ++i) {
+          const bool interior = i >= 1 && i < N && j >= 1 && j < N && k >= 1 && k < N;
+          if (!interior) lut_h[(k * N1 + j) * N1 + i] = nshell++;
+        }
+    for (int c2 = 0; c2 < N; ++c2)
+      for (int b2 = 0; b2 < N; ++b2)
+        for (int a2 = 0; a2 < N; ++a2)
+          if (a2 == N - 1 || b2 == N - 1 || c2 == N - 1) sh_h.push_back(a2 + N * (b2 + N * c2));
+    nshared = static_cast<int>(sh_h.size());
+    lut.upload(lut_h);
+    shared.upload(sh_h);
+    // basis
+    std::vector<double> xih(N1), wh(N1), Dh(N1 * N1);
+    host_gll(N, xih.data(), wh.data());
+    host_deriv_matrix(N, xih.data(), Dh.data());
+    xi.alloc(N1);
+    w.alloc(N1);
+    Dm.alloc(N1 * N1);
+    CMG_CUDA(cudaMemcpy(xi.p, xih.data(), N1 * sizeof(double), cudaMemcpyHostToDevice));
+    CMG_CUDA(cudaMemcpy(w.p, wh.data(), N1 * sizeof(double), cudaMemcpyHostToDevice));
+    CMG_CUDA(cudaMemcpy(Dm.p, Dh.data(), N1 * N1 * sizeof(double), cudaMemcpyHostToDevice));
+    cudaStream_t s = ctx->stream;
+    // geometry on the device (setup)
+    G.alloc(static_cast<std::size_t>(E) * 6 * NP);
+    Lrhs.alloc(static_cast<std::size_t>(E) * NP);
+    SemGeom g{N, Ex, Ey, Ez, z0, Ezl, d.geometry, d.eps, xi.p, w.p, Dm.p};
+    sem_geometry(g, G.p, Lrhs.p, nullptr, s);
+    shell.alloc(static_cast<std::size_t>(E) * nshell);
+    halo_lo.alloc(static_cast<std::size_t>(Ex) * Ey * N * N);
+    halo_send.alloc(static_cast<std::size_t>(Ex) * Ey * N * N);
+    contrib_hi.alloc(static_cast<std::size_t>(Ex) * Ey * N1 * N1);
+    contrib_send.alloc(static_cast<std::size_t>(Ex) * Ey * N1 * N1);
+    halo_lo.zero(s);
+    contrib_hi.zero(s);
+    // assembled diagonal (App. A5) and the padding mask
+    {
+      DBuf Ld(static_cast<std::size_t>(E) * NP);
+      sem_local_diag(N, E, G.p, Dm.p, Ld.p, s);
+      diagv.alloc(len);
+      diagv.zero(s);
+      SemArgs a = args();
+      a.lvec = Ld.p;
+      a.y = diagv.p;
+      run(SEM_LVEC, EPI_STORE, a);
+      ctx->sync();
+    }
+    mask.alloc(len);
+    sem_slot_mask(args(), mask.p, s);
+    // per-layer reduction buffers (up to 64 vectors)
+    lpart.alloc(static_cast<std::size_t>(64) * Ezl * 16);
+    lout.alloc(static_cast<std::size_t>(64) * Ezl);
+    lgath.alloc(static_cast<std::size_t>(64) * Ez);
+    lpr_h.assign(d.nranks, 0);
+    for (int r = 0; r < d.nranks; ++r) {
+      cmg_sem_desc dr = d;
+      dr.rank = r;
+      int a0, a1;
+      partition(dr, a0, a1);
+      lpr_h[r] = a1 - a0;
+    }
+    lpr.upload(lpr_h);
+    ctx->sync();
+  }
+
+  SemArgs args() const {
+    SemArgs a;
+    a.N = N;
+    a.Ex = Ex;
+    a.Ey = Ey;
+    a.Ezl = Ezl;
+    a.Ez = Ez;
+    a.z0 = z0;
+    a.E = E;
+    a.G = G.p;
+    a.D = Dm.p;
+    a.lut = lut.p;
+    a.shared = shared.p;
+    a.nshared = nshared;
+    a.nshell = nshell;
+    a.shell = shell.p;
+    a.halo_lo = halo_lo.p;
+    a.contrib_hi = contrib_hi.p;
+    a.e_begin = 0;
+    a.e_end = E;
+    return a;
+  }
+
+  bool distributed() const { return desc.nranks > 1; }
+  int up() const { return desc.rank + 1 < desc.nranks ? desc.rank + 1 : -1; }
+  int down() const { return desc.rank > 0 ? desc.rank - 1 : -1; }
+
+  // input face halo: my top layer (c=N-1 slots) goes up, the layer below comes in
+  void exchange_halo(const double* u) {
+    if (!distributed()) return;
+    SemArgs a = args();
+    sem_pack_top(a, u, halo_send.p, ctx->stream);
+    ctx->comm->sendrecv(halo_send.p, halo_send.n, halo_lo.p, halo_lo.n, up(), down(), ctx->stream);
+  }
+  // shell contributions of my bottom face go down, the layer above's come in
+  void exchange_contrib() {
+    if (!distributed()) return;
+    SemArgs a = args();
+    sem_pack_contrib_bottom(a, contrib_send.p, ctx->stream);
+    ctx->comm->sendrecv(contrib_send.p, contrib_send.n, contrib_hi.p, contrib_hi.n, down(), up(),
+                        ctx->stream);
+  }
+
+  void run(int mode, int epi, SemArgs& a) {
+    if (mode == SEM_AX) exchange_halo(a.u);
+    sem_k1(a, mode, epi, ctx->stream);
+    exchange_contrib();
+    sem_k2(a, epi, ctx->stream);
+  }
+
+  void apply(const double* x, double* y) override {
+    SemArgs a = args();
+    a.u = x;
+    a.y = y;
+    run(SEM_AX, EPI_STORE, a);
+    ++count;
+  }
+  void residual(const double* b, const double* x, double* r) override {
+    SemArgs a = args();
+    a.u = x;
+    a.b = b;
+    a.r = r;
+    run(SEM_AX, EPI_RESID, a);
+    ++count;
+  }
+  void diagonal(double* d) override {
+    CMG_CUDA(cudaMemcpyAsync(d, diagv.p, len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  void cheb4_init(const double* b, const double* x, bool xz, const double* invd, double c0,
+                  double* r, double* d) override {
+    if (xz) {
+      sem_cheb4_init_zero(len, b, invd, c0, r, d, ctx->stream);
+      return;
+    }
+    SemArgs a = args();
+    a.u = x;
+    a.b = b;
+    a.r = r;
+    a.d_out = d;
+    a.invd = invd;
+    a.c0 = c0;
+    run(SEM_AX, EPI_CHEB4_INIT, a);
+    ++count;
+  }
+  void cheb4_step(double beta, double c1, double c2, bool xz, const double* invd,
+                  const double* r_in, double* x, double* r, const double* d, double* d_out) override {
+    SemArgs a = args();
+    a.u = d;
+    a.d = d;
+    a.d_out = d_out;
+    a.x = x;
+    a.r = r;
+    a.r_in = r_in;
+    a.invd = invd;
+    a.beta = beta;
+    a.c1 = c1;
+    a.c2 = c2;
+    a.x_zero = xz ? 1 : 0;
+    run(SEM_AX, EPI_CHEB4, a);
+    ++count;
+  }
+  void cheb1_init(const double* b, const double* x, bool xz, const double* invd, double theta,
+                  double* z, double* d) override {
+    if (xz) {
+      sem_cheb1_init_zero(len, b, invd, theta, z, d, ctx->stream);
+      return;
+    }
+    SemArgs a = args();
+    a.u = x;
+    a.b = b;
+    a.r = z;
+    a.d_out = d;
+    a.invd = invd;
+    a.theta = theta;
+    run(SEM_AX, EPI_CHEB1_INIT, a);
+    ++count;
+  }
+  void cheb1_step(double c1, double c2, bool xz, const double* invd, double* x, double* z,
+                  const double* d, double* d_out) override {
+    SemArgs a = args();
+    a.u = d;
+    a.d = d;
+    a.d_out = d_out;
+    a.x = x;
+    a.r = z;
+    a.invd = invd;
+    a.c1 = c1;
+    a.c2 = c2;
+    a.x_zero = xz ? 1 : 0;
+    run(SEM_AX, EPI_CHEB1, a);
+    ++count;
+  }
+
+  // deterministic, partition-independent inner products (sem_kernels.hpp)
+  void layer_reduce(const double* V, std::size_t ldv, int nv, const double* w, double* out,
+                    bool do_sqrt) {
+    if (nv > 64) fail(CMG_EINVAL, "sem: too many vectors in one reduction");
+    const long layer_len = static_cast<long>(Ex) * Ey * N * N * N;
+    sem_layer_dots(V, ldv, nv, w, layer_len, Ezl, lpart.p, lout.p, ctx->stream);
+    const double* g = lout.p;
+    if (distributed()) {
+      ctx->comm->allgather(lout.p, lgath.p, static_cast<std::size_t>(nv) * Ezl, ctx->stream);
+      g = lgath.p;
+    }
+    sem_layer_finalize(g, nv, lpr.p, desc.nranks, out, do_sqrt ? 1 : 0, ctx->stream);
+  }
+  void dot(const double* a, const double* b, double* out) override { layer_reduce(a, 0, 1, b, out, false); }
+  void norm2(const double* a, double* out) override { layer_reduce(a, 0, 1, a, out, true); }
+  void mdot(const double* V, std::size_t ldv, int nv, const double* w, double* out) override {
+    layer_reduce(V, ldv, nv, w, out, false);
+  }
+
+  std::vector<long> slot_map() const {
+    std::vector<long> m(len);
+    for (std::size_t q = 0; q < len; ++q) m[q] = canonical_of_slot(desc, z0, static_cast<long>(q));
+    return m;
+  }
+  void upload_canonical(const double* host, double* dev) override {
+    std::vector<double> h(len, 0.0);
+    const auto m = slot_map();
+    for (std::size_t q = 0; q < len; ++q)
+      if (m[q] >= 0) h[q] = host[m[q]];
+    CMG_CUDA(cudaMemcpyAsync(dev, h.data(), len * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+  }
+  void download_canonical(const double* dev, double* host) override {
+    std::vector<double> h(len);
+    CMG_CUDA(cudaMemcpyAsync(h.data(), dev, len * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    const auto m = slot_map();
+    for (std::size_t q = 0; q < len; ++q)
+      if (m[q] >= 0) host[m[q]] = h[q];
+  }
+
+  void rhs(double* b) {
+    SemArgs a = args();
+    a.lvec = Lrhs.p;
+    a.y = b;
+    CMG_CUDA(cudaMemsetAsync(b, 0, len * sizeof(double), ctx->stream));
+    run(SEM_LVEC, EPI_STORE, a);
+  }
+};
+
+// ============================================================== p-multigrid
+struct cmg_pmg {
+  cmg_ctx* ctx = nullptr;
+  int nlevels = 0;
+  int smoother = 0;
+  std::vector<std::unique_ptr<SemLevel>> lev;
+  std::vector<std::unique_ptr<DBuf>> invd, J, Lc, vr, vb, vx;
+  std::vector<double> lambda;
+  // coarse FDM (p=1 box): S_d, lam_d per dimension, D grid over the full p=1 slot array
+  DBuf Sx, Sy, Sz, Dg, cfull, t1, t2;
+  int cnx = 0, cny = 0, cnz = 0;
+};
+
+namespace {
+
+void pmg_restrict(cmg_pmg* p, int l, const double* xf, double* yc) {
+  SemLevel* f = p->lev[l].get();
+  SemLevel* c = p->lev[l + 1].get();
+  sem_restrict_local(f->args(), c->N, p->J[l]->p, xf, p->Lc[l]->p, p->ctx->stream);
+  SemArgs a = c->args();
+  a.lvec = p->Lc[l]->p;
+  a.y = yc;
+  c->run(SEM_LVEC, EPI_STORE, a);
+}
+
+void pmg_prolong(cmg_pmg* p, int l, const double* xc, double* yf, bool add) {
+  SemLevel* f = p->lev[l].get();
+  SemLevel* c = p->lev[l + 1].get();
+  c->exchange_halo(xc);
+  sem_prolong(f->args(), c->args(), p->J[l]->p, xc, yf, add, p->ctx->stream);
+}
+
+// exact p=1 solve on the box: A_1^{-1} = (Sz x Sy x Sx) D^{-1} (Sz x Sy x Sx)^T
+void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
+  SemLevel* c = p->lev.back().get();
+  cudaStream_t s = p->ctx->stream;
+  if (c->N != 1) fail(CMG_EINVAL, "pmg: the coarsest level must be p=1");
+  const long full = static_cast<long>(c->Ex) * c->Ey * c->Ez;
+  const double* in = rc;
+  if (c->distributed()) {
+    p->ctx->comm->allgather(rc, p->cfull.p, c->len, s);
+    in = p->cfull.p;
+  }
+  const int nx = p->cnx, ny = p->cny, nz = p->cnz;
+  const long s1 = c->Ex, s2 = static_cast<long>(c->Ex) * c->Ey;
+  if (nx < 1 || ny < 1 || nz < 1) {  // no interior p=1 unknowns
+    CMG_CUDA(cudaMemsetAsync(ec, 0, c->len * sizeof(double), s));
+    return;
+  }
+  CMG_CUDA(cudaMemsetAsync(p->t1.p, 0, full * sizeof(double), s));
+  CMG_CUDA(cudaMemsetAsync(p->t2.p, 0, full * sizeof(double), s));
+  mode_product(0, nx, ny, nz, s1, s2, p->Sx.p, nx, true, in, p->t1.p, nullptr, s);
+  mode_product(1, nx, ny, nz, s1, s2, p->Sy.p, ny, true, p->t1.p, p->t2.p, nullptr, s);
+  mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, true, p->t2.p, p->t1.p, p->Dg.p, s);
+  mode_product(0, nx, ny, nz, s1, s2, p->Sx.p, nx, false, p->t1.p, p->t2.p, nullptr, s);
+  mode_product(1, nx, ny, nz, s1, s2, p->Sy.p, ny, false, p->t2.p, p->t1.p, nullptr, s);
+  if (c->distributed()) {
+    mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, false, p->t1.p, p->t2.p, nullptr, s);
+    CMG_CUDA(cudaMemcpyAsync(ec, p->t2.p + static_cast<long>(c->z0) * s2, c->len * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+  } else {
+    CMG_CUDA(cudaMemsetAsync(ec, 0, c->len * sizeof(double), s));
+    mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, false, p->t1.p, ec, nullptr, s);
+  }
+}
+
+void pmg_smooth(cmg_pmg* p, int l, const cmg_cheb_config& cfg, std::size_t order, const double* b,
+                double* x, bool xz) {
+  chebyshev_smooth(p->lev[l].get(), p->invd[l]->p, cfg, order, b, x, xz);
+}
+
+// multigrid.hpp:69-90, recursively over the p-levels
+void pmg_vcycle(cmg_pmg* p, int l, const cmg_cycle_config& cc, const double* b, double* x, bool xz) {
+  SemLevel* L = p->lev[l].get();
+  cudaStream_t s = p->ctx->stream;
+  if (l == p->nlevels - 1) {
+    if (xz) {
+      pmg_coarse_solve(p, b, x);
+    } else {
+      L->residual(b, x, p->vr[l]->p);
+      pmg_coarse_solve(p, p->vr[l]->p, p->vx[l]->p);
+      launch_axpy(L->len, 1.0, p->vx[l]->p, x, s);
+    }
+    return;
+  }
+  cmg_cheb_config cfg = cc.smoother;
+  cfg.lambda_tilde = p->lambda[l];
+  if (cc.k_pre > 0) {
+    pmg_smooth(p, l, cfg, cc.k_pre, b, x, xz);
+    xz = false;
+  }
+  const double* r = b;
+  if (!xz) {
+    L->residual(b, x, p->vr[l]->p);
+    r = p->vr[l]->p;
+  }
+  double* bc = p->vb[l + 1]->p;
+  double* xc = p->vx[l + 1]->p;
+  pmg_restrict(p, l, r, bc);
+  CMG_CUDA(cudaMemsetAsync(xc, 0, p->lev[l + 1]->len * sizeof(double), s));
+  pmg_vcycle(p, l + 1, cc, bc, xc, true);
+  pmg_prolong(p, l, xc, x, !xz);
+  if (cc.k_post > 0) pmg_smooth(p, l, cfg, cc.k_post, b, x, false);
+}
+
+struct PmgPrecond final : cmg_precond {
+  cmg_pmg* p = nullptr;
+  cmg_cycle_config cfg{};
+  void apply(const double* v, double* z) override {
+    CMG_CUDA(cudaMemsetAsync(z, 0, p->lev[0]->len * sizeof(double), ctx->stream));
+    pmg_vcycle(p, 0, cfg, v, z, true);
+  }
+};
+
+SemLevel* as_sem(cmg_op* op) {
+  auto* s = dynamic_cast<SemLevel*>(op);
+  if (!s) fail(CMG_EINVAL, "operator is not a SEM operator");
+  return s;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+int cmg_sem_partition(const cmg_sem_desc* d, int* z0, int* z1) {
+  return guard([&] {
+    validate_desc(*d);
+    partition(*d, *z0, *z1);
+  });
+}
+
+size_t cmg_sem_local_slots(const cmg_sem_desc* d) {
+  int z0, z1;
+  partition(*d, z0, z1);
+  return static_cast<size_t>(d->ex) * d->ey * (z1 - z0) * d->order * d->order * d->order;
+}
+
+int cmg_sem_slot_map_host(const cmg_sem_desc* d, int64_t* map) {
+  return guard([&] {
+    validate_desc(*d);
+    int z0, z1;
+    partition(*d, z0, z1);
+    const std::size_t len = cmg_sem_local_slots(d);
+    for (std::size_t q = 0; q < len; ++q) map[q] = canonical_of_slot(*d, z0, static_cast<long>(q));
+  });
+}
+
+int cmg_sem_gs_map_host(const cmg_sem_desc* d, int64_t* map) {
+  return guard([&] {
+    validate_desc(*d);
+    int z0, z1;
+    partition(*d, z0, z1);
+    const int N = d->order, N1 = N + 1;
+    const long NP = static_cast<long>(N1) * N1 * N1;
+    const long Mx = static_cast<long>(N) * d->ex - 1, My = static_cast<long>(N) * d->ey - 1;
+    const long E = static_cast<long>(d->ex) * d->ey * (z1 - z0);
+    for (long e = 0; e < E; ++e) {
+      const int ex = static_cast<int>(e % d->ex), ey = static_cast<int>((e / d->ex) % d->ey);
+      const int ez = z0 + static_cast<int>(e / (static_cast<long>(d->ex) * d->ey));
+      for (int k = 0; k < N1; ++k)
+        for (int j = 0; j < N1; ++j)
+          for (int i = 0; i < N1; ++i) {
+            const long gx = static_cast<long>(ex) * N + i, gy = static_cast<long>(ey) * N + j,
+                       gz = static_cast<long>(ez) * N + k;
+            const bool dir = gx == 0 || gx == static_cast<long>(N) * d->ex || gy == 0 ||
+                             gy == static_cast<long>(N) * d->ey || gz == 0 || gz == static_cast<long>(N) * d->ez;
+            map[e * NP + (k * N1 + j) * N1 + i] = dir ? -1 : ((gz - 1) * My + (gy - 1)) * Mx + (gx - 1);
+          }
+    }
+  });
+}
+
+int cmg_sem_op_create(cmg_ctx* c, const cmg_sem_desc* d, cmg_op** out) {
+  return guard([&] { *out = new SemLevel(c, *d); });
+}
+
+int cmg_sem_rhs(cmg_op* op, double* b) {
+  return guard([&] { as_sem(op)->rhs(b); });
+}
+
+int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const int* orders,
+                   int smoother, size_t eigen_iterations, uint64_t eigen_seed, cmg_pmg** out) {
+  return guard([&] {
+    if (nlevels < 2 || nlevels > 6) fail(CMG_EINVAL, "pmg: need 2..6 levels");
+    if (orders[0] != fine->order) fail(CMG_EINVAL, "pmg: orders[0] must equal the fine order");
+    for (int l = 1; l < nlevels; ++l)
+      if (orders[l] >= orders[l - 1]) fail(CMG_EINVAL, "pmg: orders must decrease");
+    if (orders[nlevels - 1] != 1) fail(CMG_EINVAL, "pmg: the coarsest level must be p=1");
+    if (smoother != 0) fail(CMG_EINVAL, "pmg: Schwarz smoothers are not built yet");
+    if (fine->geometry != 0) fail(CMG_EINVAL, "pmg: deformed-mesh coarse solve not built yet");
+    auto p = std::make_unique<cmg_pmg>();
+    p->ctx = ctx;
+    p->nlevels = nlevels;
+    p->smoother = smoother;
+    cudaStream_t s = ctx->stream;
+    for (int l = 0; l < nlevels; ++l) {
+      cmg_sem_desc d = *fine;
+      d.order = orders[l];
+      p->lev.push_back(std::make_unique<SemLevel>(ctx, d));
+      SemLevel* L = p->lev.back().get();
+      auto iv = std::make_unique<DBuf>(L->len);
+      int* zf = ctx->dflag + 11;
+      CMG_CUDA(cudaMemsetAsync(zf, 0, sizeof(int), s));
+      sem_inverse_diag(L->args(), L->diagv.p, iv->p, zf, s);
+      p->invd.push_back(std::move(iv));
+      for (auto* v : {&p->vr, &p->vb, &p->vx}) {
+        v->push_back(std::make_unique<DBuf>(L->len));
+        v->back()->zero(s);
+      }
+    }
+    for (int l = 0; l + 1 < nlevels; ++l) {
+      const int Nf = orders[l], Nc = orders[l + 1];
+      std::vector<double> Jh((Nf + 1) * (Nc + 1));
+      host_interp_matrix(Nf, Nc, Jh.data());
+      p->J.push_back(std::make_unique<DBuf>(Jh.size()));
+      CMG_CUDA(cudaMemcpy(p->J.back()->p, Jh.data(), Jh.size() * sizeof(double), cudaMemcpyHostToDevice));
+      p->Lc.push_back(std::make_unique<DBuf>(static_cast<std::size_t>(p->lev[l]->E) * (Nc + 1) * (Nc + 1) *
+                                             (Nc + 1)));
+    }
+    // coarse separable eigenbases (p=1 on the uniform box: K = tridiag(-1,2,-1)/h, M = h I)
+    SemLevel* C = p->lev.back().get();
+    auto eig1d = [&](int ne, DBuf& S, std::vector<double>& lam) {
+      const int m = ne - 1;
+      lam.assign(std::max(m, 1), 0.0);
+      S.alloc(std::max(m * m, 1));
+      if (m < 1) return;
+      const double h = 1.0 / ne;
+      std::vector<double> K(m * m, 0.0), M(m * m, 0.0), Sh(m * m);
+      for (int i = 0; i < m; ++i) {
+        K[i * m + i] = 2.0 / h;
+        if (i > 0) K[i * m + i - 1] = -1.0 / h;
+        if (i + 1 < m) K[i * m + i + 1] = -1.0 / h;
+        M[i * m + i] = h;
+      }
+      host_sym_geneig(m, K.data(), M.data(), Sh.data(), lam.data());
+      CMG_CUDA(cudaMemcpy(S.p, Sh.data(), m * m * sizeof(double), cudaMemcpyHostToDevice));
+    };
+    std::vector<double> lx, ly, lz;
+    eig1d(C->Ex, p->Sx, lx);
+    eig1d(C->Ey, p->Sy, ly);
+    eig1d(C->Ez, p->Sz, lz);
+    p->cnx = C->Ex - 1;
+    p->cny = C->Ey - 1;
+    p->cnz = C->Ez - 1;
+    const long full = static_cast<long>(C->Ex) * C->Ey * C->Ez;
+    std::vector<double> Dh(full, 1.0);
+    for (int k = 0; k < p->cnz; ++k)
+      for (int j = 0; j < p->cny; ++j)
+        for (int i = 0; i < p->cnx; ++i)
+          Dh[i + static_cast<long>(C->Ex) * (j + static_cast<long>(C->Ey) * k)] = lx[i] + ly[j] + lz[k];
+    p->Dg.alloc(full);
+    CMG_CUDA(cudaMemcpy(p->Dg.p, Dh.data(), full * sizeof(double), cudaMemcpyHostToDevice));
+    p->cfull.alloc(full);
+    p->t1.alloc(full);
+    p->t2.alloc(full);
+    p->cfull.zero(s);
+    // lambda_tilde per smoothed level (smoothers.hpp:61-79 with S = invD)
+    p->lambda.assign(nlevels, 0.0);
+    for (int l = 0; l + 1 < nlevels; ++l) {
+      p->lambda[l] = estimate_lambda_max(p->lev[l].get(), p->invd[l]->p, eigen_iterations, eigen_seed);
+      p->lev[l]->count = 0;
+    }
+    ctx->sync();
+    *out = p.release();
+  });
+}
+
+int cmg_pmg_destroy(cmg_pmg* p) {
+  return guard([&] { delete p; });
+}
+cmg_op* cmg_pmg_op(cmg_pmg* p, int level) { return p->lev.at(level).get(); }
+double cmg_pmg_lambda_tilde(const cmg_pmg* p, int level) { return p->lambda.at(level); }
+const double* cmg_pmg_inv_diag(cmg_pmg* p, int level) { return p->invd.at(level)->p; }
+
+int cmg_pmg_prolong(cmg_pmg* p, int level, const double* xc, double* yf) {
+  return guard([&] { pmg_prolong(p, level, xc, yf, false); });
+}
+int cmg_pmg_restrict(cmg_pmg* p, int level, const double* xf, double* yc) {
+  return guard([&] { pmg_restrict(p, level, xf, yc); });
+}
+int cmg_pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
+  return guard([&] { pmg_coarse_solve(p, rc, ec); });
+}
+int cmg_pmg_schwarz_apply(cmg_pmg* p, int level, const double* r, double* out) {
+  return guard([&] {
+    (void)p; (void)level; (void)r; (void)out;
+    fail(CMG_EINVAL, "pmg: Schwarz smoothers are not built yet");
+  });
+}
+int cmg_pmg_smooth(cmg_pmg* p, int level, const cmg_cheb_config* cfg, size_t order, const double* b,
+                   double* x, int x_is_zero) {
+  return guard([&] { pmg_smooth(p, level, *cfg, order, b, x, x_is_zero != 0); });
+}
+int cmg_pmg_v_cycle(cmg_pmg* p, const cmg_cycle_config* cfg, const double* b, double* x, int x_is_zero) {
+  return guard([&] { pmg_vcycle(p, 0, *cfg, b, x, x_is_zero != 0); });
+}
+int cmg_precond_pmg(cmg_pmg* p, const cmg_cycle_config* cfg, cmg_precond** out) {
+  return guard([&] {
+    auto m = std::make_unique<PmgPrecond>();
+    m->ctx = p->ctx;
+    m->p = p;
+    m->cfg = *cfg;
+    *out = m.release();
+  });
+}
+
+}  // extern "C"

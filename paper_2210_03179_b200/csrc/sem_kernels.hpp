@@ -1,0 +1,125 @@
+// sem_kernels.hpp -- launch interface of the SEM kernels (k_sem.cu).
+//
+// Vector layout ("owned slots"): element e = ex + Ex*(ey + Ey*ez)
+// (ez local to the rank's z-slab) owns the GLL nodes with local indices
+// (a+1, b+1, c+1), a,b,c in [0,N); slot = e*N^3 + a + N*(b + N*c).  Slots on
+// the far domain boundary are padding (kept zero).  A node with some local
+// index 0 is owned by the -x/-y/-z neighbour; Dirichlet nodes are eliminated.
+//
+// QQ^T (direct stiffness summation) is split in two deterministic kernels:
+//   K1 (element kernel): computes the local contribution at all (N+1)^3 nodes
+//       of each element; nodes interior to the element (all indices in
+//       1..N-1, single contributor) are finished in place with the fused
+//       epilogue; the "shell" nodes are written to a shell buffer.
+//   K2 (shared-node kernel): every owned node with some local index == N sums
+//       its <= 8 contributions in a FIXED (dz,dy,dx) order -- the same order on
+//       every partition, so results are bitwise independent of the GPU count --
+//       and applies the same epilogue.
+#pragma once
+
+#include "cmg_internal.hpp"
+
+namespace cmg {
+
+enum SemMode : int { SEM_AX = 0, SEM_LVEC = 1 };
+enum SemEpi : int {
+  EPI_STORE = 0,      // y = w
+  EPI_RESID = 1,      // r = b - w
+  EPI_CHEB4 = 2,      // x += beta d ; r = r_in - w ; d_out = c1 d + c2 invd r
+  EPI_CHEB1 = 3,      // x += d ; z -= invd w ; d_out = c1 d + c2 z
+  EPI_CHEB4_INIT = 4, // r = b - w ; d_out = c0 invd r
+  EPI_CHEB1_INIT = 5, // z = invd (b - w) ; d_out = z / theta
+  EPI_ADD = 6         // y += w
+};
+
+struct SemArgs {
+  int N = 7;
+  int Ex = 1, Ey = 1, Ezl = 1;  // local element grid (Ezl element layers on this rank)
+  int Ez = 1, z0 = 0;           // global layers, first global layer of this rank
+  long E = 1;                   // local elements
+  const double* G = nullptr;    // [E][6][(N+1)^3]
+  const double* D = nullptr;    // (N+1)^2
+  const int* lut = nullptr;     // local node -> shell index (-1 interior)
+  const int* shared = nullptr;  // shared-owned slot list (slot-local index)
+  int nshared = 0, nshell = 0;
+  double* shell = nullptr;      // [E][nshell]
+  const double* u = nullptr;    // AX input (slots)
+  const double* lvec = nullptr; // LVEC input [E][(N+1)^3]
+  const double* halo_lo = nullptr;    // [Ex*Ey*N*N] slots c=N-1 of the layer below (other rank)
+  const double* contrib_hi = nullptr; // [Ex*Ey*(N+1)^2] k=0 contributions of the layer above
+  // epilogue operands (slot vectors)
+  double* y = nullptr;
+  const double* b = nullptr;
+  double* x = nullptr;
+  double* r = nullptr;
+  const double* r_in = nullptr;
+  const double* d = nullptr;
+  double* d_out = nullptr;
+  const double* invd = nullptr;
+  double beta = 1, c1 = 0, c2 = 0, c0 = 0, theta = 1;
+  int x_zero = 0;
+  // element range [e_begin, e_end) processed by this launch (for overlap splits)
+  long e_begin = 0, e_end = 0;
+};
+
+// K1 over elements [e_begin, e_end) and K2 over the same elements
+void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s);
+void sem_k2(const SemArgs& a, int epi, cudaStream_t s);
+
+// pointwise epilogues over all slots (x_is_zero smoother inits)
+void sem_cheb4_init_zero(std::size_t n, const double* b, const double* invd, double c0, double* r,
+                         double* d, cudaStream_t s);
+void sem_cheb1_init_zero(std::size_t n, const double* b, const double* invd, double theta,
+                         double* z, double* d, cudaStream_t s);
+
+// halo packing
+void sem_pack_top(const SemArgs& a, const double* u, double* buf, cudaStream_t s);
+void sem_pack_contrib_bottom(const SemArgs& a, double* buf, cudaStream_t s);
+
+// setup: geometric factors (and optional RHS L-vector B f), per element
+struct SemGeom {
+  int N, Ex, Ey, Ez, z0, Ezl;
+  int geometry;  // 0 box, 1 Kershaw
+  double eps;
+  const double* xi;  // GLL nodes (device)
+  const double* w;   // weights (device)
+  const double* D;   // derivative matrix (device)
+};
+void sem_geometry(const SemGeom& g, double* G, double* Lrhs, double* Lmass, cudaStream_t s);
+// local diagonal of A_e into an L-vector
+void sem_local_diag(int N, long E, const double* G, const double* D, double* Ldiag, cudaStream_t s);
+// invd = valid ? 1/diag : 0  ; flags zero diagonal entries on valid slots
+void sem_inverse_diag(const SemArgs& a, const double* diag, double* invd, int* zero_flag,
+                      cudaStream_t s);
+// slot validity mask (1.0 valid, 0.0 padding)
+void sem_slot_mask(const SemArgs& a, double* mask, cudaStream_t s);
+
+// p-transfers between two levels on the same element grid
+// prolong: y_f (=|+=) J^{(x)3} x_c at owned fine slots; coarse gather uses halo_lo (coarse)
+void sem_prolong(const SemArgs& fine, const SemArgs& coarse, const double* J, const double* xc,
+                 double* yf, bool add, cudaStream_t s);
+// restrict (first half): coarse L-vector = J^T^{(x)3} (fine owned values, zero elsewhere)
+void sem_restrict_local(const SemArgs& fine, int Nc, const double* J, const double* xf,
+                        double* Lc, cudaStream_t s);
+
+// per-layer partial inner products: out[v*Ezl + l] = sum over layer l of V_v . w
+void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
+                    int nlayers, double* partials, double* out, cudaStream_t s);
+// final sum over all global layers (gathered [rank][v][layer_local] blocks) in z order
+void sem_layer_finalize(const double* gathered, int nv, const int* layers_per_rank, int nranks,
+                        double* out, int do_sqrt, cudaStream_t s);
+
+// Schwarz (ASM/RAS) with FDM local solves
+struct SchwarzArgs {
+  int N, Ex, Ey, Ezl, Ez, z0;
+  const double* S;    // [E][3][pb*pb]   (column eigenvectors, S^T B S = I)
+  const double* lam;  // [E][3][pb]
+  const double* r;    // input residual (slots)
+  const double* halo_lo;  // [Ex*Ey*N*N*2]: two top layers (c=N-1, N-2) of the layer below
+  const double* halo_hi;  // [Ex*Ey*N*N*2]? (c=0,1) of the layer above
+  double* Lout;       // output local (ras: (N+1)^3 per element; asm: (N+3)^3)
+  int ras;
+};
+void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s);
+
+}  // namespace cmg

@@ -288,3 +288,205 @@ def hexs(xs) -> list[str]:
 
 def unhex(xs) -> np.ndarray:
     return np.array([float.fromhex(s) for s in xs])
+
+
+# ---------------------------------------------------------------- SEM (restated spec; parity unpinned)
+def _sem_protos(L):
+    L.orc_sem_create.restype = C.c_void_p
+    L.orc_sem_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double]
+    L.orc_sem_destroy.argtypes = [C.c_void_p]
+    L.orc_sem_n.restype = sz
+    L.orc_sem_n.argtypes = [C.c_void_p]
+    L.orc_sem_op.restype = C.c_void_p
+    L.orc_sem_op.argtypes = [C.c_void_p]
+    L.orc_op_apply.argtypes = [C.c_void_p, dp, dp]
+    L.orc_sem_diagonal.argtypes = [C.c_void_p, dp]
+    L.orc_sem_rhs.argtypes = [C.c_void_p, dp]
+    L.orc_sem_local_to_global_map.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    L.orc_sem_geom.argtypes = [C.c_void_p, dp, dp]
+    L.orc_sem_prolong.argtypes = [C.c_void_p, C.c_void_p, dp, dp]
+    L.orc_sem_restrict.argtypes = [C.c_void_p, C.c_void_p, dp, dp]
+    L.orc_sem_schwarz.argtypes = [C.c_void_p, C.c_int, dp, dp]
+    L.orc_gll.argtypes = [C.c_int, dp, dp]
+    L.orc_deriv_matrix.argtypes = [C.c_int, dp, dp]
+    L.orc_interp_matrix.argtypes = [C.c_int, C.c_int, dp]
+    L.orc_pmg_create.restype = C.c_void_p
+    L.orc_pmg_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                 C.c_int, sz, C.c_uint64]
+    L.orc_pmg_destroy.argtypes = [C.c_void_p]
+    L.orc_pmg_op.restype = C.c_void_p
+    L.orc_pmg_op.argtypes = [C.c_void_p, C.c_int]
+    L.orc_pmg_sem.restype = C.c_void_p
+    L.orc_pmg_sem.argtypes = [C.c_void_p, C.c_int]
+    L.orc_pmg_lambda_tilde.restype = C.c_double
+    L.orc_pmg_lambda_tilde.argtypes = [C.c_void_p, C.c_int]
+    L.orc_pmg_v_cycle.restype = C.c_int
+    L.orc_pmg_v_cycle.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, sz, sz, dp, dp, C.c_int]
+    L.orc_pmg_coarse_solve.argtypes = [C.c_void_p, dp, dp]
+    L.orc_pmg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, sz, sz, dp, C.c_double, sz,
+                                sz, dp, dp, C.POINTER(_Rep)]
+    L.orc_chebyshev_smooth.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_CCfg), sz, dp, dp, C.c_int]
+    L.orc_estimate_lambda_max.restype = C.c_double
+    L.orc_estimate_lambda_max.argtypes = [C.c_void_p, C.c_void_p, sz, C.c_uint64]
+
+
+class _Smoother(C.Structure):
+    _fields_ = [("inv_diag", dp), ("S_apply", C.c_void_p), ("S_ctx", C.c_void_p)]
+
+
+class OracleSem:
+    """Restated SEM operator on one level (canonical interior ordering)."""
+
+    def __init__(self, N, ex, ey, ez, geometry=0, eps=1.0, lib=None):
+        self.L = lib or oracle()
+        _sem_protos(self.L)
+        self.N, self.ex, self.ey, self.ez = N, ex, ey, ez
+        self.s = self.L.orc_sem_create(N, ex, ey, ez, geometry, eps)
+        if not self.s:
+            raise ValueError("orc_sem_create failed")
+        self.n = self.L.orc_sem_n(self.s)
+        self._own = True
+
+    def __del__(self):
+        if getattr(self, "_own", False) and self.s:
+            self.L.orc_sem_destroy(self.s)
+
+    def apply(self, x):
+        y = np.empty(self.n)
+        self.L.orc_op_apply(self.L.orc_sem_op(self.s), P(np.ascontiguousarray(x)), P(y))
+        return y
+
+    def diagonal(self):
+        d = np.empty(self.n)
+        self.L.orc_sem_diagonal(self.s, P(d))
+        return d
+
+    def rhs(self):
+        b = np.empty(self.n)
+        self.L.orc_sem_rhs(self.s, P(b))
+        return b
+
+    def gs_map(self):
+        m = np.empty(self.ex * self.ey * self.ez * (self.N + 1) ** 3, dtype=np.int64)
+        self.L.orc_sem_local_to_global_map(self.s, m.ctypes.data_as(C.POINTER(C.c_int64)))
+        return m
+
+    def geom(self):
+        E, NP = self.ex * self.ey * self.ez, (self.N + 1) ** 3
+        G, B = np.empty(E * 6 * NP), np.empty(E * NP)
+        self.L.orc_sem_geom(self.s, P(G), P(B))
+        return G, B
+
+    def schwarz(self, r, ras):
+        out = np.empty(self.n)
+        self.L.orc_sem_schwarz(self.s, 1 if ras else 0, P(np.ascontiguousarray(r)), P(out))
+        return out
+
+
+def gll(N):
+    xi, w = np.empty(N + 1), np.empty(N + 1)
+    L = oracle()
+    _sem_protos(L)
+    L.orc_gll(N, P(xi), P(w))
+    D = np.empty((N + 1) ** 2)
+    L.orc_deriv_matrix(N, P(xi), P(D))
+    return xi, w, D.reshape(N + 1, N + 1)
+
+
+def interp_matrix(Nf, Nc):
+    L = oracle()
+    _sem_protos(L)
+    J = np.empty((Nf + 1) * (Nc + 1))
+    L.orc_interp_matrix(Nf, Nc, P(J))
+    return J.reshape(Nf + 1, Nc + 1)
+
+
+class OraclePmg:
+    """Restated p-multigrid hierarchy; `lib` may be the _ref library (reference templates)."""
+
+    def __init__(self, orders, ex, ey, ez, geometry=0, eps=1.0, smoother=0, eig_iters=30, seed=7, lib=None):
+        self.L = lib or oracle()
+        _sem_protos(self.L)
+        self.orders = list(orders)
+        arr = (C.c_int * len(orders))(*orders)
+        self.p = self.L.orc_pmg_create(len(orders), arr, ex, ey, ez, geometry, eps, smoother, eig_iters, seed)
+        if not self.p:
+            raise ValueError("orc_pmg_create failed")
+        self.lambda_tilde = [self.L.orc_pmg_lambda_tilde(self.p, l) for l in range(len(orders))]
+        self.n = [self.L.orc_sem_n(self.L.orc_pmg_sem(self.p, l)) for l in range(len(orders))]
+
+    def __del__(self):
+        if getattr(self, "p", None):
+            self.L.orc_pmg_destroy(self.p)
+
+    def sem(self, level):
+        s = OracleSem.__new__(OracleSem)
+        s.L = self.L
+        s.s = self.L.orc_pmg_sem(self.p, level)
+        s.n = self.n[level]
+        s._own = False
+        return s
+
+    def v_cycle(self, family, kpre, kpost, b, lmaxm=1.03, lminm=0.1):
+        x = np.zeros(self.n[0])
+        rc = self.L.orc_pmg_v_cycle(self.p, family, lmaxm, lminm, kpre, kpost, P(np.ascontiguousarray(b)), P(x), 1)
+        assert rc == 0
+        return x
+
+    def coarse_solve(self, rc):
+        e = np.empty_like(rc)
+        self.L.orc_pmg_coarse_solve(self.p, P(np.ascontiguousarray(rc)), P(e))
+        return e
+
+    def prolong(self, level, xc):
+        y = np.empty(self.n[level])
+        self.L.orc_sem_prolong(self.L.orc_pmg_sem(self.p, level), self.L.orc_pmg_sem(self.p, level + 1),
+                               P(np.ascontiguousarray(xc)), P(y))
+        return y
+
+    def restrict(self, level, xf):
+        y = np.empty(self.n[level + 1])
+        self.L.orc_sem_restrict(self.L.orc_pmg_sem(self.p, level), self.L.orc_pmg_sem(self.p, level + 1),
+                                P(np.ascontiguousarray(xf)), P(y))
+        return y
+
+    def smooth(self, level, family, order, b, x, x_is_zero, lmaxm=1.03, lminm=0.1, inv_diag=None):
+        s = self.sem(level)
+        invd = 1.0 / s.diagonal() if inv_diag is None else inv_diag
+        sm = _Smoother(P(invd), None, None)
+        cfg = _CCfg(family, self.lambda_tilde[level], lmaxm, lminm)
+        x = np.array(x, dtype=np.float64)
+        rc = self.L.orc_chebyshev_smooth(self.L.orc_pmg_op(self.p, level), C.byref(sm), C.byref(cfg), order,
+                                         P(np.ascontiguousarray(b)), P(x), 1 if x_is_zero else 0)
+        assert rc == 0
+        return x
+
+    def solve(self, driver, family, kpre, kpost, b, tol=1e-8, maxit=500, restart=30, lmaxm=1.03, lminm=0.1):
+        x = np.zeros(self.n[0])
+        hist = np.zeros(maxit + 2)
+        rep = _Rep()
+        self.L.orc_pmg_solve(self.p, driver, family, lmaxm, lminm, kpre, kpost, P(np.ascontiguousarray(b)), tol,
+                             maxit, restart, P(x), P(hist), C.byref(rep))
+        return Report(int(rep.iterations), int(rep.fine_matvecs), hist[: rep.hist_len].tolist(), bool(rep.converged),
+                      rep.status.decode(), float(rep.rho), wall_time_sec=float(rep.wall), x=x)
+
+
+def ref_sem_solve(pmg: OraclePmg, driver, family, kpre, kpost, b, tol=1e-8, maxit=500, restart=30):
+    """The reference's own pcg/pgmres templates driving the restated SEM operator
+    (oracle/ref_driver.cpp); `pmg` must have been created with lib=ref()."""
+    R = ref()
+    R.ref_sem_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, sz, sz, dp, C.c_double, sz,
+                                sz, dp, dp, sz, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz), C.POINTER(C.c_int),
+                                C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    x = np.zeros(pmg.n[0])
+    hist = np.zeros(maxit + 2)
+    hl, its, mv = sz(), sz(), sz()
+    cv = C.c_int()
+    st = C.create_string_buffer(128)
+    rho, wall = C.c_double(), C.c_double()
+    rc = R.ref_sem_solve(pmg.p, driver, family, 1.03, 0.1, kpre, kpost, P(np.ascontiguousarray(b)), tol, maxit,
+                         restart, P(x), P(hist), maxit + 2, C.byref(hl), C.byref(its), C.byref(mv), C.byref(cv), st,
+                         C.byref(rho), C.byref(wall))
+    assert rc == 0, R.ref_last_error()
+    return Report(its.value, mv.value, hist[: hl.value].tolist(), bool(cv.value), st.value.decode(), rho.value,
+                  wall_time_sec=wall.value, x=x)

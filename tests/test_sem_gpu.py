@@ -1,0 +1,136 @@
+"""SEM p-multigrid path on the GPU vs the oracle restatement (and the reference's
+own Krylov templates driving it, oracle/_ref).  Tolerances in fp64: operator /
+transfer / smoother outputs 1e-12..1e-11 relative (different but fixed
+summation order), solve histories 1e-10 relative (BASELINE north_star),
+iteration counts exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_bind as ob
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def cm():
+    from paper_2210_03179_b200 import chebmg
+
+    return chebmg
+
+
+@pytest.fixture(scope="module")
+def sem():
+    from paper_2210_03179_b200 import sem
+
+    return sem
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+@pytest.mark.parametrize("N,ex,ey,ez,geo", [(7, 3, 2, 4, 0), (7, 2, 3, 2, 1), (3, 4, 3, 2, 0), (1, 5, 4, 3, 0),
+                                            (5, 2, 2, 3, 1), (2, 3, 3, 3, 0)])
+def test_apply_diag_rhs(sem, N, ex, ey, ez, geo):
+    d = sem.SemDesc(N, ex, ey, ez, geometry=geo, eps=0.3)
+    A = sem.SemOperator(d)
+    o = ob.OracleSem(N, ex, ey, ez, geo, 0.3)
+    assert A.rows() == o.n
+    x = ob.random_vector(o.n, 17)
+    y = A.new_vector()
+    A.apply(A.from_canonical(x), y)
+    assert A.applications() == 1
+    assert rel(A.to_canonical(y), o.apply(x)) <= 1e-12
+    assert rel(A.to_canonical(A.diagonal()), o.diagonal()) <= 1e-12
+    assert rel(A.to_canonical(A.rhs()), o.rhs()) <= 1e-12
+    # padding slots stay exactly zero
+    assert torch.all(y.cpu()[torch.from_numpy(~A.valid)] == 0)
+
+
+def test_sweeps_all_families(cm, sem):
+    d = sem.SemDesc(7, 3, 2, 2, geometry=1, eps=0.3)
+    P = sem.PMGHierarchy(d, (7, 3, 1))
+    o = ob.OraclePmg((7, 3, 1), 3, 2, 2, 1, 0.3)
+    for l in (0, 1):
+        assert abs(P.lambda_tilde[l] - o.lambda_tilde[l]) <= 1e-11 * o.lambda_tilde[l]
+    A = P.ops[0]
+    b = ob.random_vector(o.n[0], 3)
+    x0 = ob.random_vector(o.n[0], 4)
+    for fam in (0, 1, 2, 3):
+        for order, xz in ((1, True), (4, True), (5, False), (8, False)):
+            cfg = cm.ChebyshevConfig(cm.Family(fam), order, o.lambda_tilde[0])
+            x = A.from_canonical(np.zeros(o.n[0]) if xz else x0)
+            A.reset_applications()
+            cm.chebyshev_smooth(A, P.inv_diag(0), cfg, order, A.from_canonical(b), x, xz)
+            assert A.applications() == (order - 1 if xz else order)
+            ref = o.smooth(0, fam, order, b, np.zeros(o.n[0]) if xz else x0, xz)
+            assert rel(A.to_canonical(x), ref) <= 1e-11, (fam, order, xz)
+
+
+def test_transfers_and_coarse_solve(sem):
+    for geo in (0, 1):
+        d = sem.SemDesc(7, 4, 3, 3, geometry=geo, eps=0.3)
+        P = sem.PMGHierarchy(d, (7, 3, 1)) if geo == 0 else None
+        if P is None:
+            continue
+        o = ob.OraclePmg((7, 3, 1), 4, 3, 3, geo, 0.3)
+        for l in (0, 1):
+            xc = ob.random_vector(o.n[l + 1], 5)
+            xf = ob.random_vector(o.n[l], 6)
+            Pc, Pf = P.ops[l + 1], P.ops[l]
+            assert rel(Pf.to_canonical(P.prolong(l, Pc.from_canonical(xc))), o.prolong(l, xc)) <= 1e-13
+            assert rel(Pc.to_canonical(P.restrict(l, Pf.from_canonical(xf))), o.restrict(l, xf)) <= 1e-13
+        rc = ob.random_vector(o.n[2], 7)
+        C1 = P.ops[2]
+        assert rel(C1.to_canonical(P.coarse_solve(C1.from_canonical(rc))), o.coarse_solve(rc)) <= 1e-11
+
+
+@pytest.mark.parametrize("fam,kpre,kpost", [(2, 4, 0), (3, 4, 0), (0, 2, 2), (2, 2, 2)])
+def test_v_cycle(cm, sem, fam, kpre, kpost):
+    d = sem.SemDesc(7, 3, 3, 2)
+    P = sem.PMGHierarchy(d, (7, 3, 1))
+    o = ob.OraclePmg((7, 3, 1), 3, 3, 2)
+    b = o.sem(0).rhs()
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, 1.0), kpre, kpost)
+    P.A.reset_applications()
+    z = P.preconditioner_apply(cyc, P.A.from_canonical(b))
+    assert P.A.applications() == kpre + kpost
+    assert rel(P.A.to_canonical(z), o.v_cycle(fam, kpre, kpost, b)) <= TOL
+
+
+@pytest.mark.parametrize("fam,kpre,kpost,driver", [(2, 4, 0, "pgmres"), (3, 4, 0, "pgmres"), (0, 2, 2, "pgmres"),
+                                                   (2, 2, 2, "pcg"), (2, 8, 0, "pgmres")])
+def test_pmg_solves_match_reference_templates(cm, sem, fam, kpre, kpost, driver):
+    """p-MG(7,3,1)-preconditioned PGMRES/PCG (tol 1e-8): GPU vs the
+    reference's own pcg/pgmres templates driving the restated SEM operator."""
+    ex, ey, ez = 4, 3, 3
+    d = sem.SemDesc(7, ex, ey, ez)
+    P = sem.PMGHierarchy(d, (7, 3, 1))
+    R = ob.ref if ob.ref_available() else None
+    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, lib=R() if R else None)
+    b = o.sem(0).rhs()
+    drv = {"pcg": 0, "pgmres": 1}[driver]
+    oref = ob.ref_sem_solve(o, drv, fam, kpre, kpost, b, tol=1e-8) if R else o.solve(drv, fam, kpre, kpost, b)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
+    fn = cm.pgmres if driver == "pgmres" else cm.pcg
+    x, rep = fn(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
+    assert (rep.iterations, rep.fine_matvecs, rep.status) == (oref.iterations, oref.fine_matvecs, oref.status)
+    h, hr = np.array(rep.residual_history), np.array(oref.history)
+    assert np.max(np.abs(h - hr) / hr) <= TOL
+    assert rel(P.A.to_canonical(x), oref.x) <= TOL
+
+
+def test_determinism(cm, sem):
+    d = sem.SemDesc(7, 3, 3, 3)
+    P = sem.PMGHierarchy(d, (7, 3, 1))
+    b = P.A.rhs()
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 4, 0)
+    r1 = cm.pgmres(P.A, P.preconditioner(cyc), b, None, cm.SolveOptions(tol=1e-8))[1]
+    r2 = cm.pgmres(P.A, P.preconditioner(cyc), b, None, cm.SolveOptions(tol=1e-8))[1]
+    assert r1.residual_history == r2.residual_history
+
+
+def test_smoke_check(sem):
+    assert "SEM" in sem.smoke_check()
