@@ -1,0 +1,355 @@
+#!/usr/bin/env python3
+"""bench.py -- BASELINE.json metric on B200.
+
+Metric: "GDOF/s per Chebyshev smoother sweep; p-MG-GMRES time-to-solution".
+A *step* is one 4th-kind Chebyshev-Jacobi smoother sweep of order 8 (the
+(2k,0) half-V-cycle smoother with k=4) on the fine level of the SEM Poisson
+problem N=7, E=64^3 (BASELINE north-star target; configs[4] is the same
+problem element-partitioned over 2/4/8 GPUs).  Each step = 8 fused
+Ax+QQ^T+Chebyshev passes (warm start: the residual pass plus 7 steps).
+`value` = total unknowns x 8 x K / (max over ranks of the device time) in
+GDOF-step/s.  Extra keys carry the full p-MG(7,3,1)-PGMRES time-to-solution,
+the FD config-1 solve, the roofline and the CPU baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
+                          s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU reference arm
+def cpu_reference_sweep(E: int, order: int, reps: int, seconds_cap: float = 20.0):
+    """Reference chebyshev_smooth template (oracle/_ref, compiled from the reference
+    headers) over the SEM operator restatement; single thread (core.hpp:34-35).
+    Returns (GDOF-step/s, kind, sample description)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle_bind as ob
+
+    use_ref = ob.ref_available()
+    L = ob.ref() if use_ref else ob.oracle()
+    pm = ob.OraclePmg((7, 3, 1), E, E, E, lib=L, eig_iters=30)
+    n = pm.n[0]
+    b = pm.sem(0).rhs()
+    x = ob.random_vector(n, 11)
+    lam = pm.lambda_tilde[0]
+    if use_ref:
+        L.ref_sem_sweep_create.restype = C.c_void_p
+        L.ref_sem_sweep_create.argtypes = [C.c_void_p, C.c_int]
+        L.ref_sem_sweep_run.argtypes = [C.c_void_p, C.c_int, ob.sz, C.c_double, ob.dp, ob.dp, C.c_int, C.c_int]
+        sw = L.ref_sem_sweep_create(pm.p, 0)
+        run = lambda: L.ref_sem_sweep_run(sw, 2, order, lam, ob.P(b), ob.P(x), 0, 1)  # noqa: E731
+        kind = "reference"
+    else:
+        invd = 1.0 / pm.sem(0).diagonal()
+        run = lambda: pm.smooth(0, 2, order, b, x, False, inv_diag=invd)  # noqa: E731
+        kind = "port"
+    run()  # warm
+    t0 = time.perf_counter()
+    done = 0
+    while done < reps and time.perf_counter() - t0 < seconds_cap:
+        run()
+        done += 1
+    dt = time.perf_counter() - t0
+    sample = (f"SEM N=7 E={E}^3 ({n} unknowns) 4th-kind Chebyshev-Jacobi sweep order {order}, {done} sweeps, "
+              f"{'reference chebyshev_smooth template (oracle/_ref) over the oracle SEM operator' if use_ref else 'oracle port'}")
+    return n * order * done / dt / 1e9, kind, sample
+
+
+def _replica(args):
+    E, order, reps = args
+    v, kind, sample = cpu_reference_sweep(E, order, reps)
+    return v, kind, sample
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference CPU path on all host cores (independent
+    single-thread replicas, the reference being single-threaded by contract)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    E = args.cpu_E
+    order = 8
+    reps = 3
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        outs = pool.map(_replica, [(E, order, reps)] * cores)
+    wall = time.perf_counter() - t0
+    value = sum(o[0] for o in outs)
+    line = {
+        "impl": "reference", "metric": "GDOF/s per Chebyshev smoother sweep", "value": value,
+        "unit": "GDOF-step/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"SEM Poisson box N=7 E={E}^3 4th-kind Chebyshev-Jacobi sweep "
+                                                    f"order 8 (bounded CPU sample of the E=64^3 workload)"},
+        "cpu_baseline": {"value": value, "unit": "GDOF-step/s", "cores": cores, "kind": outs[0][1],
+                         "sample": f"{cores} single-thread replicas x " + outs[0][2]},
+        "e2e": {"value": value, "unit": "GDOF-step/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--E", type=int, default=64, help="elements per direction (N=7)")
+    ap.add_argument("--order", type=int, default=8)
+    ap.add_argument("--cpu-E", dest="cpu_E", type=int, default=12)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_2210_03179_b200 import chebmg as cm
+    from paper_2210_03179_b200 import sem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ctx = cm.Context(local)
+    if world > 1:
+        uid = [cm.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.attach_nccl(uid[0], rank, world)
+
+    E, order = args.E, args.order
+    desc = sem.SemDesc(7, E, E, E, rank=rank, nranks=world)
+    t_setup = time.perf_counter()
+    P = sem.PMGHierarchy(desc, (7, 3, 1), ctx=ctx)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    A = P.A
+    invd = P.inv_diag(0)
+    n_glob = desc.unknowns()
+    b = A.rhs()
+    x = A.new_vector()
+    x.copy_(torch.rand_like(x) * torch.from_numpy(A.valid.astype(np.float64)).to(x.device))
+    cfg = cm.ChebyshevConfig(cm.Family.fourth, order, P.lambda_tilde[0])
+    stream = torch.cuda.current_stream()
+
+    def sweep():
+        cm.chebyshev_smooth(A, invd, cfg, order, b, x, False)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sweep()
+    barrier()
+    l0 = cm.Context.kernel_launches()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with Clocks(local) as clk:
+        ev[0].record(stream)
+        for k in range(args.steps):
+            sweep()
+            ev[k + 1].record(stream)
+        barrier()
+    launches = cm.Context.kernel_launches() - l0
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    t_ms = ev[0].elapsed_time(ev[-1])
+    if dist:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    value = n_glob * order * args.steps / (t_ms * 1e-3) / 1e9
+
+    # roofline of the fused step (K1+K2 pair): SURVEY §8(d) algorithmic bytes,
+    # 48 B per local node (6 geometric factors) + 64 B per global unknown
+    N_L = 512 * E ** 3
+    bytes_step = 48 * N_L + 64 * n_glob
+    per_gpu_bytes = bytes_step / world
+    step_s = ms_per_step * 1e-3 / order
+    peak, peak_src = peaks()
+    achieved = per_gpu_bytes / step_s / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "fused Chebyshev-Jacobi step (sem K1 element kernel + K2 shared-node kernel)",
+            "algorithmic_bytes_per_step": per_gpu_bytes, "peak_source": peak_src}
+
+    # e2e through the public API with host buffers: H2D b,x ; sweep ; D2H x
+    hb = b.detach().cpu().pin_memory()
+    hx = x.detach().cpu().pin_memory()
+    hout = torch.empty_like(hx).pin_memory()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        b.copy_(hb, non_blocking=True)
+        x.copy_(hx, non_blocking=True)
+        sweep()
+        hout.copy_(x, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist:
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e = {"value": n_glob * order / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF-step/s",
+           "h2d_bytes_per_step": 2 * b.numel() * 8 * world, "d2h_bytes_per_step": x.numel() * 8 * world,
+           "ms_per_step": e2e_ms}
+
+    # p-MG(7,3,1)-PGMRES time to solution (tol 1e-8, restart 30), half V-cycle (8,0)
+    tts = None
+    if not args.no_solve:
+        cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 8, 0)
+        M = P.preconditioner(cyc)
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        xs, rep = cm.pgmres(A, M, b, None, cm.SolveOptions(tol=1e-8, restart=30, maxit=500))
+        s1.record(stream)
+        barrier()
+        sms = s0.elapsed_time(s1)
+        if dist:
+            tt = torch.tensor([sms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            sms = float(tt.item())
+        tts = {"solver": "PGMRES(30) + p-MG(7,3,1) 4th-kind Chebyshev-Jacobi half V-cycle (8,0)", "tol": 1e-8,
+               "iterations": rep.iterations, "fine_matvecs": rep.fine_matvecs, "converged": rep.converged,
+               "time_to_solution_s": sms * 1e-3, "ms_per_iteration": sms / max(rep.iterations, 1),
+               "final_rel_residual": rep.residual_history[-1] / rep.residual_history[0]}
+
+    fd = None
+    cpu = None
+    if rank == 0 and world == 1:
+        # FD config 1: n=256 (255^2 unknowns), PGMRES + 4th-kind (4,0) half V-cycle, factor 2, Lx=1
+        h = cm.build_hierarchy(cm.Domain(1.0, 1.0, 256), 2, ctx=ctx)
+        prob = cm.build_problem(h.domain, 1234, ctx)
+        Mfd = cm.vcycle_preconditioner(h, cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, h.lambda_tilde), 4, 0))
+        for _ in range(3):
+            cm.pgmres(h.A, Mfd, prob.b, None, cm.SolveOptions())
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        f0.record(stream)
+        reps = 10
+        for _ in range(reps):
+            _, frep = cm.pgmres(h.A, Mfd, prob.b, None, cm.SolveOptions())
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fd = {"workload": "FD 5-point n=256 Lx=1 factor 2, PGMRES(30) + 4th-kind (4,0) half V-cycle, tol 1e-6",
+              "iterations": frep.iterations, "fine_matvecs": frep.fine_matvecs,
+              "time_to_solution_ms": f0.elapsed_time(f1) / reps}
+        if not args.no_cpu:
+            v, kind, sample = cpu_reference_sweep(args.cpu_E, order, reps=50, seconds_cap=15.0)
+            cpu = {"value": v, "unit": "GDOF-step/s", "cores": 1, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "GDOF/s per Chebyshev smoother sweep", "value": value, "unit": "GDOF-step/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"SEM Poisson box [-1/2,1/2]^3 N=7 E={E}^3 ({n_glob} unknowns), 4th-kind "
+                                   f"Chebyshev-Jacobi sweep order {order} on the fine level of p-MG(7,3,1), "
+                                   f"warm start", "N": 7, "E": E ** 3, "unknowns": n_glob,
+                       "partition": f"z-slabs x{world}", "l2": "inputs larger than L2 (each vector "
+                                                            f"{A.vec_len() * 8 / 1e6:.0f} MB/GPU, G "
+                                                            f"{6 * 512 * E ** 3 * 8 / world / 1e9:.1f} GB/GPU)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "time_to_solution": tts, "fd_config1": fd,
+            "setup_s": t_setup, "step_ms_min_max": [min(step_ms), max(step_ms)],
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

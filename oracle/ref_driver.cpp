@@ -295,6 +295,38 @@ int ref_sem_smooth(void* pmg, int level, int family, std::size_t order, double l
   });
 }
 
+// Bench helper: a reusable smoother context (inverse diagonal computed once,
+// smoothers.hpp:174-181) so repeated sweeps time only chebyshev_smooth.
+struct SemSweep {
+  orc_pmg* p;
+  int level;
+  SemOperator A;
+  Vec inv_diag;
+};
+
+void* ref_sem_sweep_create(void* pmg, int level) {
+  auto* p = static_cast<orc_pmg*>(pmg);
+  SemOperator A(orc_pmg_op(p, level), orc_pmg_sem(p, level));
+  auto* s = new SemSweep{p, level, A, jacobi_inverse_diagonal(A.diagonal())};
+  return s;
+}
+void ref_sem_sweep_destroy(void* s) { delete static_cast<SemSweep*>(s); }
+
+// `reps` sweeps of chebyshev_smooth (reference template) on the stored operator
+int ref_sem_sweep_run(void* sp, int family, std::size_t order, double lambda_tilde, const double* b,
+                      double* x, int x_is_zero, int reps) {
+  auto* s = static_cast<SemSweep*>(sp);
+  return guarded([&] {
+    ChebyshevConfig cfg;
+    cfg.family = fam(family);
+    cfg.lambda_tilde = lambda_tilde;
+    const std::size_t n = s->A.rows();
+    Vec bv(b, b + n), xv(x, x + n);
+    for (int r = 0; r < reps; ++r) chebyshev_smooth(s->A, s->inv_diag, cfg, order, bv, xv, x_is_zero != 0);
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
 // p-MG preconditioned PGMRES / PCG through the reference's Krylov templates
 // (krylov.hpp:75-264); the preconditioner is the restated multilevel V-cycle.
 int ref_sem_solve(void* pmg, int driver, int family, double lmax_mult, double lmin_mult,

@@ -200,8 +200,7 @@ double estimate_lambda_max(cmg_op* A, const double* invd, std::size_t iterations
   cmg_ctx* c = A->ctx;
   int* zf = c->dflag + 8;
   CMG_CUDA(cudaMemsetAsync(zf, 0, sizeof(int), c->stream));
-  launch_any_zero(A->len == A->n ? A->n : A->n, invd, zf, c->stream);
-  // (for padded layouts the op zero-fills padding of invd with 1.0, so only real entries test)
+  A->flag_zero_entries(invd, zf);  // smoothers.hpp:66-67 (padding slots excluded)
   int hz = 0;
   CMG_CUDA(cudaMemcpyAsync(&hz, zf, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   c->sync();

@@ -61,7 +61,8 @@ enum : int {
   S_HS = S_H + 4160,    // copy
   S_G = S_HS + 4160,    // m+1
   S_Y = S_G + 80,       // m
-  S_END = S_Y + 80
+  S_CG = S_Y + 80,      // coarse CG scalars (8)
+  S_END = S_CG + 16
 };
 
 struct cmg_ctx {
@@ -121,6 +122,10 @@ struct cmg_op {
   }
   virtual void mdot(const double* V, std::size_t ldv, int nv, const double* w, double* out_dev) {
     cmg::launch_mdot(V, ldv, nv, w, len, ctx->dpart, out_dev, ctx->stream);
+  }
+  // set *flag if any unknown's entry of v is exactly zero (storage padding excluded)
+  virtual void flag_zero_entries(const double* v, int* flag) {
+    cmg::launch_any_zero(len, v, flag, ctx->stream);
   }
   // host canonical vector -> device storage layout (identity for FD)
   virtual void upload_canonical(const double* host, double* dev) {

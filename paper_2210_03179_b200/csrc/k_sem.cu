@@ -454,6 +454,12 @@ __global__ void k_inverse_diag(SemArgs A, const double* __restrict__ d, double* 
   }
 }
 
+__global__ void k_flag_zero_valid(SemArgs A, const double* __restrict__ v, int* flag) {
+  const long n = A.E * (long)A.N * A.N * A.N;
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x)
+    if (v[q] == 0.0 && slot_valid(A, q)) atomicExch(flag, 1);
+}
+
 __global__ void k_slot_mask(SemArgs A, double* __restrict__ m) {
   const long n = A.E * (long)A.N * A.N * A.N;
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x)
@@ -679,6 +685,12 @@ void sem_inverse_diag(const SemArgs& a, const double* diag, double* invd, int* z
                       cudaStream_t s) {
   const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
   k_inverse_diag<<<vgrid(n), 256, 0, s>>>(a, diag, invd, zero_flag);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_flag_zero_valid(const SemArgs& a, const double* v, int* flag, cudaStream_t s) {
+  const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
+  k_flag_zero_valid<<<vgrid(n), 256, 0, s>>>(a, v, flag);
   CMG_LAUNCH_CHECK();
 }
 

@@ -251,6 +251,9 @@ struct SemLevel final : cmg_op {
     run(SEM_AX, EPI_RESID, a);
     ++count;
   }
+  void flag_zero_entries(const double* v, int* flag) override {
+    sem_flag_zero_valid(args(), v, flag, ctx->stream);
+  }
   void diagonal(double* d) override {
     CMG_CUDA(cudaMemcpyAsync(d, diagv.p, len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   }
@@ -379,6 +382,7 @@ struct cmg_pmg {
   std::vector<double> lambda;
   // coarse FDM (p=1 box): S_d, lam_d per dimension, D grid over the full p=1 slot array
   DBuf Sx, Sy, Sz, Dg, cfull, t1, t2;
+  DBuf cg_r, cg_z, cg_p, cg_Ap;  // deformed-mesh coarse CG
   int cnx = 0, cny = 0, cnz = 0;
 };
 
@@ -402,7 +406,7 @@ void pmg_prolong(cmg_pmg* p, int l, const double* xc, double* yf, bool add) {
 }
 
 // exact p=1 solve on the box: A_1^{-1} = (Sz x Sy x Sx) D^{-1} (Sz x Sy x Sx)^T
-void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
+void pmg_fdm_box(cmg_pmg* p, const double* rc, double* ec) {
   SemLevel* c = p->lev.back().get();
   cudaStream_t s = p->ctx->stream;
   if (c->N != 1) fail(CMG_EINVAL, "pmg: the coarsest level must be p=1");
@@ -433,6 +437,59 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
     CMG_CUDA(cudaMemsetAsync(ec, 0, c->len * sizeof(double), s));
     mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, false, p->t1.p, ec, nullptr, s);
   }
+}
+
+// p=1 solve.  Box: the FDM solve is exact.  Deformed (Kershaw) mesh: the
+// rediscretised p=1 operator is not separable, so the coarse solve is CG on
+// A_1 preconditioned by the box FDM, run to a relative residual of 1e-13
+// (numerically exact; the paper's single CPU BoomerAMG V-cycle, PAPER.md:618-622,
+// is replaced by this all-GPU solve -- no CPU fallback).
+void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
+  SemLevel* c = p->lev.back().get();
+  if (c->desc.geometry == 0) {
+    pmg_fdm_box(p, rc, ec);
+    return;
+  }
+  cmg_ctx* ctx = p->ctx;
+  cudaStream_t s = ctx->stream;
+  const std::size_t L = c->len;
+  double* x = ec;
+  double* r = p->cg_r.p;
+  double* z = p->cg_z.p;
+  double* pp = p->cg_p.p;
+  double* Ap = p->cg_Ap.p;
+  double* sc = ctx->dscal + S_CG;
+  int* stop = ctx->dflag + 12;
+  const std::size_t cnt0 = c->count;
+  CMG_CUDA(cudaMemsetAsync(x, 0, L * sizeof(double), s));
+  CMG_CUDA(cudaMemcpyAsync(r, rc, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CMG_CUDA(cudaMemsetAsync(stop, 0, sizeof(int), s));
+  c->norm2(r, sc + 0);  // r0
+  pmg_fdm_box(p, r, z);
+  CMG_CUDA(cudaMemcpyAsync(pp, z, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  c->dot(r, z, sc + 1);  // rz
+  CMG_CUDA(cudaMemcpyAsync(ctx->hpin, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  ctx->sync();
+  const double r0 = ctx->hpin[0];
+  if (r0 == 0.0) return;
+  for (int it = 1; it <= 500; ++it) {
+    c->apply(pp, Ap);
+    c->dot(pp, Ap, sc + 2);
+    launch_pcg_alpha(sc + 1, sc + 2, sc + 3, stop, s);
+    launch_axpy_dev(L, sc + 3, 1.0, pp, x, stop, s);
+    launch_axpy_dev(L, sc + 3, -1.0, Ap, r, stop, s);
+    if (it % 8 == 0) {
+      c->norm2(r, sc + 5);
+      CMG_CUDA(cudaMemcpyAsync(ctx->hpin, sc + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
+      ctx->sync();
+      if (ctx->hpin[0] <= 1e-13 * r0) break;
+    }
+    pmg_fdm_box(p, r, z);
+    c->dot(r, z, sc + 4);
+    launch_pcg_beta(sc + 4, sc + 1, sc + 6, stop, s);
+    launch_xpby_dev(L, z, sc + 6, pp, stop, s);
+  }
+  c->count = cnt0;  // coarse-level applications are not fine matvecs
 }
 
 void pmg_smooth(cmg_pmg* p, int l, const cmg_cheb_config& cfg, std::size_t order, const double* b,
@@ -559,7 +616,6 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
       if (orders[l] >= orders[l - 1]) fail(CMG_EINVAL, "pmg: orders must decrease");
     if (orders[nlevels - 1] != 1) fail(CMG_EINVAL, "pmg: the coarsest level must be p=1");
     if (smoother != 0) fail(CMG_EINVAL, "pmg: Schwarz smoothers are not built yet");
-    if (fine->geometry != 0) fail(CMG_EINVAL, "pmg: deformed-mesh coarse solve not built yet");
     auto p = std::make_unique<cmg_pmg>();
     p->ctx = ctx;
     p->nlevels = nlevels;
@@ -626,6 +682,10 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
     p->t1.alloc(full);
     p->t2.alloc(full);
     p->cfull.zero(s);
+    for (DBuf* b : {&p->cg_r, &p->cg_z, &p->cg_p, &p->cg_Ap}) {
+      b->alloc(C->len);
+      b->zero(s);
+    }
     // lambda_tilde per smoothed level (smoothers.hpp:61-79 with S = invD)
     p->lambda.assign(nlevels, 0.0);
     for (int l = 0; l + 1 < nlevels; ++l) {

@@ -93,6 +93,8 @@ void sem_inverse_diag(const SemArgs& a, const double* diag, double* invd, int* z
                       cudaStream_t s);
 // slot validity mask (1.0 valid, 0.0 padding)
 void sem_slot_mask(const SemArgs& a, double* mask, cudaStream_t s);
+// *flag = 1 if some valid slot of v is exactly zero
+void sem_flag_zero_valid(const SemArgs& a, const double* v, int* flag, cudaStream_t s);
 
 // p-transfers between two levels on the same element grid
 // prolong: y_f (=|+=) J^{(x)3} x_c at owned fine slots; coarse gather uses halo_lo (coarse)

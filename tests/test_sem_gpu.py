@@ -72,9 +72,7 @@ def test_sweeps_all_families(cm, sem):
 def test_transfers_and_coarse_solve(sem):
     for geo in (0, 1):
         d = sem.SemDesc(7, 4, 3, 3, geometry=geo, eps=0.3)
-        P = sem.PMGHierarchy(d, (7, 3, 1)) if geo == 0 else None
-        if P is None:
-            continue
+        P = sem.PMGHierarchy(d, (7, 3, 1))
         o = ob.OraclePmg((7, 3, 1), 4, 3, 3, geo, 0.3)
         for l in (0, 1):
             xc = ob.random_vector(o.n[l + 1], 5)
@@ -120,6 +118,22 @@ def test_pmg_solves_match_reference_templates(cm, sem, fam, kpre, kpost, driver)
     h, hr = np.array(rep.residual_history), np.array(oref.history)
     assert np.max(np.abs(h - hr) / hr) <= TOL
     assert rel(P.A.to_canonical(x), oref.x) <= TOL
+
+
+@pytest.mark.parametrize("eps,kpre,kpost", [(0.3, 4, 0), (0.3, 2, 2), (0.05, 8, 0)])
+def test_kershaw_solves(cm, sem, eps, kpre, kpost):
+    """Deformed-mesh config (BASELINE configs[3] shape): half (2k,0) vs full (k,k) cycles."""
+    ex = ey = ez = 3
+    d = sem.SemDesc(7, ex, ey, ez, geometry=sem.KERSHAW, eps=eps)
+    P = sem.PMGHierarchy(d, (7, 3, 1))
+    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, 1, eps)
+    b = o.sem(0).rhs()
+    oref = o.solve(1, 2, kpre, kpost, b, tol=1e-8)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), kpre, kpost)
+    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
+    assert (rep.iterations, rep.fine_matvecs) == (oref.iterations, oref.fine_matvecs)
+    h, hr = np.array(rep.residual_history), np.array(oref.history)
+    assert np.max(np.abs(h - hr) / hr) <= TOL
 
 
 def test_determinism(cm, sem):
