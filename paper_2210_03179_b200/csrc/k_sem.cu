@@ -172,6 +172,211 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1(SemArgs A) {
   }
 }
 
+// ---------------------------------------------------------------- K1 (TMA-fed, AX mode)
+// Async-copy helpers (sm_90+ PTX; sm_100a SASS: UBLKCP / LDGSTS / SYNCS).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// number of slot-vector operands the epilogue reads for interior nodes
+template <int EPI>
+struct EpiOps {
+  static constexpr int n = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) ? 3
+                           : (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) ? 2
+                           : (EPI == EPI_RESID || EPI == EPI_ADD) ? 1 : 0;
+};
+
+template <int N, int EPI>
+struct K1Smem {
+  static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NO = N * N * N;
+  static constexpr int EPB = SemC<N>::EPB;
+  static constexpr int NOPS = EpiOps<EPI>::n;
+  static constexpr std::size_t g_off = 0;                                   // [EPB][6][NP]
+  static constexpr std::size_t u_off = g_off + (std::size_t)EPB * 6 * NP;   // [EPB][NP]
+  static constexpr std::size_t o_off = u_off + (std::size_t)EPB * NP;       // [NOPS][EPB][NO]
+  static constexpr std::size_t d_off = o_off + (std::size_t)NOPS * EPB * NO;  // [N1][N1+1]
+  static constexpr std::size_t bar_off = d_off + (std::size_t)N1 * (N1 + 1);
+  static constexpr std::size_t bytes = (bar_off + 1) * sizeof(double);
+};
+
+// epilogue with prefetched interior operands (slot-local index sl within element e)
+template <int EPI, int NO, int EPB>
+__device__ __forceinline__ void epilogue_pf(const SemArgs& A, long slot, int le, int sl, double w, double dv,
+                                            const double* so) {
+  const double* o0 = so + (std::size_t)le * NO;
+  const double* o1 = so + (std::size_t)(EPB + le) * NO;
+  const double* o2 = so + (std::size_t)(2 * EPB + le) * NO;
+  if constexpr (EPI == EPI_STORE) {
+    A.y[slot] = w;
+  } else if constexpr (EPI == EPI_ADD) {
+    A.y[slot] = o0[sl] + w;
+  } else if constexpr (EPI == EPI_RESID) {
+    A.r[slot] = o0[sl] - w;
+  } else if constexpr (EPI == EPI_CHEB4) {  // o0 = x, o1 = r_in, o2 = invd
+    A.x[slot] = A.x_zero ? A.beta * dv : o0[sl] + A.beta * dv;
+    const double rv = o1[sl] - w;
+    A.r[slot] = rv;
+    A.d_out[slot] = A.c1 * dv + A.c2 * o2[sl] * rv;
+  } else if constexpr (EPI == EPI_CHEB1) {  // o0 = x, o1 = z, o2 = invd
+    A.x[slot] = A.x_zero ? dv : o0[sl] + dv;
+    const double zv = o1[sl] - o2[sl] * w;
+    A.r[slot] = zv;
+    A.d_out[slot] = A.c1 * dv + A.c2 * zv;
+  } else if constexpr (EPI == EPI_CHEB4_INIT) {  // o0 = b, o1 = invd
+    const double rv = o0[sl] - w;
+    A.r[slot] = rv;
+    A.d_out[slot] = A.c0 * o1[sl] * rv;
+  } else if constexpr (EPI == EPI_CHEB1_INIT) {
+    const double zv = (o0[sl] - w) * o1[sl];
+    A.r[slot] = zv;
+    A.d_out[slot] = zv / A.theta;
+  }
+}
+
+template <int N, int EPI>
+__global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_tma(SemArgs A) {
+  using C = SemC<N>;
+  using S = K1Smem<N, EPI>;
+  constexpr int N1 = C::N1, NP = C::NP, NO = C::NO, TPE = C::TPE, EPB = C::EPB;
+  extern __shared__ __align__(128) double sm[];
+  double* sG = sm + S::g_off;
+  double* su = sm + S::u_off;
+  double* so = sm + S::o_off;
+  double (*sD)[N1 + 1] = reinterpret_cast<double (*)[N1 + 1]>(sm + S::d_off);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
+  const int le = threadIdx.x / TPE;
+  const int t = threadIdx.x - le * TPE;
+  const int i = t % N1, j = t / N1;
+  const long e0 = A.e_begin + (long)blockIdx.x * EPB;
+  const long e = e0 + le;
+  const bool active = e < A.e_end;
+  const int nact = (int)min((long)EPB, A.e_end - e0);
+  // 1. one thread streams the block's geometric factors (EPB x 24.6 KB at N=7) with TMA
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, (unsigned)(nact * 6 * NP * sizeof(double)));
+    for (int q = 0; q < nact; ++q)
+      bulk_g2s(sG + (std::size_t)q * 6 * NP, A.G + (e0 + q) * 6 * NP, 6 * NP * sizeof(double), bar);
+  }
+  for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) sD[q / N1][q % N1] = A.D[q];
+  const int ex = active ? (int)(e % A.Ex) : 0;
+  const int ey = active ? (int)((e / A.Ex) % A.Ey) : 0;
+  const int ez = active ? (int)(e / ((long)A.Ex * A.Ey)) : 0;
+  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+  // 2. async prefetch of the epilogue operands of this thread's interior column
+  if constexpr (S::NOPS > 0) {
+    if (active && ij_interior) {
+      const double* ops[3];
+      if constexpr (EPI == EPI_CHEB4) { ops[0] = A.x; ops[1] = A.r_in; ops[2] = A.invd; }
+      else if constexpr (EPI == EPI_CHEB1) { ops[0] = A.x; ops[1] = A.r; ops[2] = A.invd; }
+      else if constexpr (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) { ops[0] = A.b; ops[1] = A.invd; ops[2] = nullptr; }
+      else if constexpr (EPI == EPI_RESID) { ops[0] = A.b; ops[1] = nullptr; ops[2] = nullptr; }
+      else { ops[0] = A.y; ops[1] = nullptr; ops[2] = nullptr; }
+#pragma unroll
+      for (int q = 0; q < S::NOPS; ++q) {
+        if (q == 0 && (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero) continue;  // x not read
+#pragma unroll
+        for (int k = 1; k < N; ++k) {
+          const int sl = (i - 1) + N * ((j - 1) + N * (k - 1));
+          cp_async8(so + ((std::size_t)q * EPB + le) * NO + sl, ops[q] + e * NO + sl);
+        }
+      }
+    }
+  }
+  // 3. gather Q u (owner slots / halo / Dirichlet zero) into shared memory
+  {
+    int oex, oey;
+    const int ax = owner1d<N>(ex, i, A.Ex, oex);
+    const int ay = owner1d<N>(ey, j, A.Ey, oey);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      double v = 0.0;
+      if (active && ax >= 0 && ay >= 0) {
+        int oez;
+        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
+        if (az >= 0) {
+          const int lz = oez - A.z0;
+          if (lz < 0)
+            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
+          else
+            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NO + ax + N * (ay + N * az)];
+        }
+      }
+      su[(std::size_t)le * NP + (k * N1 + j) * N1 + i] = v;
+    }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // 4. gradient + geometric factors; w_r, w_s, w_t overwrite G_rr, G_rs, G_rt in place
+  double* Ge = sG + (std::size_t)le * 6 * NP;
+  const double* ue = su + (std::size_t)le * NP;
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    const int l = (k * N1 + j) * N1 + i;
+    double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      ur += sD[i][m] * ue[(k * N1 + j) * N1 + m];
+      us += sD[j][m] * ue[(k * N1 + m) * N1 + i];
+      ut += sD[k][m] * ue[(m * N1 + j) * N1 + i];
+    }
+    const double g0 = Ge[l], g1 = Ge[NP + l], g2 = Ge[2 * NP + l];
+    const double g3 = Ge[3 * NP + l], g4 = Ge[4 * NP + l], g5 = Ge[5 * NP + l];
+    Ge[l] = g0 * ur + g1 * us + g2 * ut;
+    Ge[NP + l] = g1 * ur + g3 * us + g4 * ut;
+    Ge[2 * NP + l] = g2 * ur + g4 * us + g5 * ut;
+  }
+  __syncthreads();
+  if (!active) return;
+  if constexpr (S::NOPS > 0) cp_async_wait_all();
+  // 5. divergence + epilogue
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      v += sD[m][i] * Ge[(k * N1 + j) * N1 + m];
+      v += sD[m][j] * Ge[NP + (k * N1 + m) * N1 + i];
+      v += sD[m][k] * Ge[2 * NP + (m * N1 + j) * N1 + i];
+    }
+    if (ij_interior && k >= 1 && k < N) {
+      const int sl = (i - 1) + N * ((j - 1) + N * (k - 1));
+      const double dv = ue[(k * N1 + j) * N1 + i];
+      epilogue_pf<EPI, NO, EPB>(A, e * NO + sl, le, sl, v, dv, so);
+    } else {
+      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K2
 template <int N, int EPI>
 __global__ void k_sem_k2(SemArgs A) {
@@ -214,7 +419,18 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
   const long blocks = (ne + C::EPB - 1) / C::EPB;
-  k_sem_k1<N, MODE, EPI><<<(unsigned)blocks, C::NT, 0, s>>>(a);
+  if constexpr (MODE == SEM_AX) {
+    constexpr std::size_t smem = K1Smem<N, EPI>::bytes;
+    static bool configured = false;
+    if (!configured) {
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_tma<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      configured = true;
+    }
+    k_sem_k1_tma<N, EPI><<<(unsigned)blocks, C::NT, smem, s>>>(a);
+  } else {
+    k_sem_k1<N, MODE, EPI><<<(unsigned)blocks, C::NT, 0, s>>>(a);
+  }
   CMG_LAUNCH_CHECK();
 }
 

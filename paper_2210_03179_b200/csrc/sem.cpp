@@ -472,17 +472,22 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
   ctx->sync();
   const double r0 = ctx->hpin[0];
   if (r0 == 0.0) return;
-  for (int it = 1; it <= 500; ++it) {
+  double last = r0;
+  for (int it = 1; it <= 2000; ++it) {
     c->apply(pp, Ap);
     c->dot(pp, Ap, sc + 2);
     launch_pcg_alpha(sc + 1, sc + 2, sc + 3, stop, s);
     launch_axpy_dev(L, sc + 3, 1.0, pp, x, stop, s);
     launch_axpy_dev(L, sc + 3, -1.0, Ap, r, stop, s);
     if (it % 8 == 0) {
+      // run to the rounding floor: stop below 1e-15 r0 or once 8 more
+      // iterations no longer halve the (recursive) residual
       c->norm2(r, sc + 5);
       CMG_CUDA(cudaMemcpyAsync(ctx->hpin, sc + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
       ctx->sync();
-      if (ctx->hpin[0] <= 1e-13 * r0) break;
+      const double rn = ctx->hpin[0];
+      if (rn <= 1e-15 * r0 || (rn <= 1e-11 * r0 && rn > 0.5 * last)) break;
+      last = rn;
     }
     pmg_fdm_box(p, r, z);
     c->dot(r, z, sc + 4);
