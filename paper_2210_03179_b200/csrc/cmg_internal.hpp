@@ -133,6 +133,9 @@ void fd_prolong(int mf, int mc, int f, const double* ec, double* x, bool assign,
 // fused: r = b - A x then rc = P^T r (r kept for nothing: computed on the fly)
 // mode product along one dim of a (n0,n1,n2) array with strides (1,s1,s2):
 //   out[..o..] = sum_m M[o*ld + m] (or M[m*ld + o] when transpose) * in[..m..]
+void mode_product_s0(int dim, int n0, int n1, int n2, long s0, long s1, long s2, const double* M,
+                     int ld, bool transpose, const double* in, double* out, const double* div,
+                     cudaStream_t s);
 void mode_product(int dim, int n0, int n1, int n2, long s1, long s2, const double* M, int ld,
                   bool transpose, const double* in, double* out, const double* div_or_null,
                   cudaStream_t s);

@@ -305,8 +305,13 @@ void fd_prolong(int mf, int mc, int f, const double* ec, double* x, bool assign,
 void mode_product(int dim, int n0, int n1, int n2, long s1, long s2, const double* M, int ld,
                   bool transpose, const double* in, double* out, const double* div,
                   cudaStream_t s) {
+  mode_product_s0(dim, n0, n1, n2, 1, s1, s2, M, ld, transpose, in, out, div, s);
+}
+
+void mode_product_s0(int dim, int n0, int n1, int n2, long s0, long s1, long s2, const double* M, int ld,
+                     bool transpose, const double* in, double* out, const double* div, cudaStream_t s) {
   const int n[3] = {n0, n1, n2};
-  const long st[3] = {1, s1, s2};
+  const long st[3] = {s0, s1, s2};
   const int a = dim == 0 ? 1 : 0, b = dim == 2 ? 1 : 2;
   const int nd = n[dim];
   const int R = n[a] * n[b];

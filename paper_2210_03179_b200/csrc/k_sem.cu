@@ -4,11 +4,19 @@
 // operator A = Q^T A_L Q (sum-factorised tensor contractions with six
 // geometric factors per node) fused with the direct
 // stiffness summation and the three-term recurrence (smoothers.hpp:126-148
-// with S = invD).  One element per (N+1)^2-thread group, one thread per
-// (i,j) column looping over k; the element's u, w_r, w_s live in shared
-// memory, u and w_t columns in registers.  See sem_kernels.hpp for the
-// K1/K2 split that makes QQ^T deterministic and partition-independent.
+// with S = invD).  See sem_kernels.hpp for the K1/K2 split that makes QQ^T
+// deterministic and partition-independent, and sem_layout.hpp for the
+// interior-first slot order that makes both kernels' vector traffic
+// contiguous per element.
+//
+// K1 (element kernel, AX mode): one element per block, (N+1)^2 x KS threads
+// ((i,j) column x k-half).  A single thread streams the element's geometric
+// factors (24.6 KB at N=7) and the interior blocks of the epilogue operands
+// into shared memory with TMA bulk copies (cp.async.bulk + mbarrier) while
+// all threads gather the input vector; w_r, w_s, w_t then overwrite the
+// factors in place, so a block needs ~34 KB and six blocks share an SM.
 #include "sem_kernels.hpp"
+#include "sem_layout.hpp"
 
 namespace cmg {
 
@@ -18,162 +26,20 @@ template <int N>
 struct SemC {
   static constexpr int N1 = N + 1;
   static constexpr int NP = N1 * N1 * N1;
-  static constexpr int NO = N * N * N;
-  static constexpr int TPE = N1 * N1;  // threads per element
+  static constexpr int NOS = sem_nos(N);
+  static constexpr int NINT = sem_nint(N);
+  static constexpr int NSH = sem_nshared(N);
+  static constexpr int KS = (N1 % 2 == 0 && N >= 3) ? 2 : 1;  // k-split across threads
+  static constexpr int KN = N1 / KS;                          // k values per thread
+  static constexpr int TPE = N1 * N1 * KS;                    // threads per element
   static constexpr int EPB = (128 / TPE) > 0 ? (128 / TPE) : 1;  // elements per block
   static constexpr int NT = EPB * TPE;
+  // interior operand block copied per element (16-byte multiple)
+  static constexpr int NINT_PAD = ((NINT * 8 + 15) / 16) * 16 / 8;
 };
 
-// ---------------------------------------------------------------- epilogue
-template <int EPI>
-__device__ __forceinline__ void epilogue(const SemArgs& A, long slot, double w, double dv) {
-  if constexpr (EPI == EPI_STORE) {
-    A.y[slot] = w;
-  } else if constexpr (EPI == EPI_ADD) {
-    A.y[slot] += w;
-  } else if constexpr (EPI == EPI_RESID) {
-    A.r[slot] = A.b[slot] - w;
-  } else if constexpr (EPI == EPI_CHEB4) {
-    // smoothers.hpp:138-144: x += beta d ; r -= A d ; d = c1 d + c2 invD r
-    A.x[slot] = A.x_zero ? A.beta * dv : A.x[slot] + A.beta * dv;
-    const double rv = A.r_in[slot] - w;
-    A.r[slot] = rv;
-    A.d_out[slot] = A.c1 * dv + A.c2 * A.invd[slot] * rv;
-  } else if constexpr (EPI == EPI_CHEB1) {
-    // smoothers.hpp:109-118: x += d ; z -= invD A d ; d = c1 d + c2 z
-    A.x[slot] = A.x_zero ? dv : A.x[slot] + dv;
-    const double zv = A.r[slot] - A.invd[slot] * w;
-    A.r[slot] = zv;
-    A.d_out[slot] = A.c1 * dv + A.c2 * zv;
-  } else if constexpr (EPI == EPI_CHEB4_INIT) {
-    const double rv = A.b[slot] - w;
-    A.r[slot] = rv;
-    A.d_out[slot] = A.c0 * A.invd[slot] * rv;
-  } else if constexpr (EPI == EPI_CHEB1_INIT) {
-    const double zv = (A.b[slot] - w) * A.invd[slot];
-    A.r[slot] = zv;
-    A.d_out[slot] = zv / A.theta;
-  }
-}
-
-// owner slot of local node index `l` (0..N) along one dimension for element coordinate `ec`:
-// returns owner element coordinate and in-element slot coordinate; -1 if Dirichlet.
-template <int N>
-__device__ __forceinline__ int owner1d(int ec, int l, int ne, int& oe) {
-  // global index g = ec*N + l ; interior iff 0 < g < N*ne
-  const int g = ec * N + l;
-  if (g <= 0 || g >= N * ne) return -1;
-  oe = (g - 1) / N;
-  return (g - 1) - oe * N;
-}
-
-// ---------------------------------------------------------------- K1
-template <int N, int MODE, int EPI>
-__global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1(SemArgs A) {
-  using C = SemC<N>;
-  constexpr int N1 = C::N1, NP = C::NP, NO = C::NO, TPE = C::TPE, EPB = C::EPB;
-  __shared__ double sD[N1][N1 + 1];
-  __shared__ double su[EPB][NP];
-  __shared__ double sr[EPB][NP];
-  __shared__ double ss[EPB][NP];
-  const int le = threadIdx.x / TPE;
-  const int t = threadIdx.x - le * TPE;
-  const int i = t % N1, j = t / N1;
-  const long e = A.e_begin + (long)blockIdx.x * EPB + le;
-  const bool active = e < A.e_end;
-  for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) sD[q / N1][q % N1] = A.D[q];
-  const int ex = active ? (int)(e % A.Ex) : 0;
-  const int ey = active ? (int)((e / A.Ex) % A.Ey) : 0;
-  const int ez = active ? (int)(e / ((long)A.Ex * A.Ey)) : 0;
-  double u[N1];
-  if constexpr (MODE == SEM_AX) {
-    // gather Q u: local (i,j,k) -> owner slot (or halo / Dirichlet zero)
-    int oex, oey;
-    const int ax = owner1d<N>(ex, i, A.Ex, oex);
-    const int ay = owner1d<N>(ey, j, A.Ey, oey);
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      double v = 0.0;
-      if (active && ax >= 0 && ay >= 0) {
-        int oez;
-        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
-        if (az >= 0) {
-          const int lz = oez - A.z0;
-          if (lz < 0) {
-            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
-          } else {
-            const long oe = (long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz);
-            v = A.u[oe * NO + ax + N * (ay + N * az)];
-          }
-        }
-      }
-      u[k] = v;
-      su[le][(k * N1 + j) * N1 + i] = v;
-    }
-  }
-  __syncthreads();
-  double out[N1];
-  if constexpr (MODE == SEM_AX) {
-    const double* Ge = A.G + (active ? e : 0) * 6 * NP;
-    double wt[N1];
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      const int l = (k * N1 + j) * N1 + i;
-      double ur = 0.0, us = 0.0, ut = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) {
-        ur += sD[i][m] * su[le][(k * N1 + j) * N1 + m];
-        us += sD[j][m] * su[le][(k * N1 + m) * N1 + i];
-        ut += sD[k][m] * u[m];
-      }
-      double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0;
-      if (active) {
-        g0 = __ldg(Ge + l);
-        g1 = __ldg(Ge + NP + l);
-        g2 = __ldg(Ge + 2 * NP + l);
-        g3 = __ldg(Ge + 3 * NP + l);
-        g4 = __ldg(Ge + 4 * NP + l);
-        g5 = __ldg(Ge + 5 * NP + l);
-      }
-      sr[le][l] = g0 * ur + g1 * us + g2 * ut;
-      ss[le][l] = g1 * ur + g3 * us + g4 * ut;
-      wt[k] = g2 * ur + g4 * us + g5 * ut;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) {
-        v += sD[m][i] * sr[le][(k * N1 + j) * N1 + m];
-        v += sD[m][j] * ss[le][(k * N1 + m) * N1 + i];
-        v += sD[m][k] * wt[m];
-      }
-      out[k] = v;
-    }
-  } else {
-    const double* Le = A.lvec + (active ? e : 0) * NP;
-#pragma unroll
-    for (int k = 0; k < N1; ++k) out[k] = active ? Le[(k * N1 + j) * N1 + i] : 0.0;
-  }
-  if (!active) return;
-  // epilogue: interior nodes finished here, shell nodes to the shell buffer
-  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
-#pragma unroll
-  for (int k = 0; k < N1; ++k) {
-    if (ij_interior && k >= 1 && k < N) {
-      const long slot = e * NO + (i - 1) + N * ((j - 1) + N * (k - 1));
-      double dv = 0.0;
-      if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) dv = u[k];
-      epilogue<EPI>(A, slot, out[k], dv);
-    } else {
-      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = out[k];
-    }
-  }
-}
-
-// ---------------------------------------------------------------- K1 (TMA-fed, AX mode)
-// Async-copy helpers (sm_90+ PTX; sm_100a SASS: UBLKCP / LDGSTS / SYNCS).
+// ---------------------------------------------------------------- async-copy helpers
+// (sm_90+ PTX; SASS on sm_100a: UBLKCP / SYNCS.* / LDGSTS)
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -201,71 +67,86 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// number of slot-vector operands the epilogue reads for interior nodes
+// owner of local node index l (0..N) along one dimension of element coordinate ec:
+// returns the owned-slot coordinate in the owner (oe) or -1 for a Dirichlet node
+template <int N>
+__device__ __forceinline__ int owner1d(int ec, int l, int ne, int& oe) {
+  const int g = ec * N + l;
+  if (g <= 0 || g >= N * ne) return -1;
+  oe = (g - 1) / N;
+  return (g - 1) - oe * N;
+}
+
+// ---------------------------------------------------------------- epilogues
 template <int EPI>
-struct EpiOps {
+struct EpiOps {  // slot-vector operands read for interior nodes, in smem order
   static constexpr int n = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) ? 3
                            : (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) ? 2
                            : (EPI == EPI_RESID || EPI == EPI_ADD) ? 1 : 0;
 };
 
-template <int N, int EPI>
-struct K1Smem {
-  static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NO = N * N * N;
-  static constexpr int EPB = SemC<N>::EPB;
-  static constexpr int NOPS = EpiOps<EPI>::n;
-  static constexpr std::size_t g_off = 0;                                   // [EPB][6][NP]
-  static constexpr std::size_t u_off = g_off + (std::size_t)EPB * 6 * NP;   // [EPB][NP]
-  static constexpr std::size_t o_off = u_off + (std::size_t)EPB * NP;       // [NOPS][EPB][NO]
-  static constexpr std::size_t d_off = o_off + (std::size_t)NOPS * EPB * NO;  // [N1][N1+1]
-  static constexpr std::size_t bar_off = d_off + (std::size_t)N1 * (N1 + 1);
-  static constexpr std::size_t bytes = (bar_off + 1) * sizeof(double);
-};
+template <int EPI>
+__device__ __forceinline__ const double* epi_op(const SemArgs& A, int q) {
+  if constexpr (EPI == EPI_CHEB4) return q == 0 ? A.x : (q == 1 ? A.r_in : A.invd);
+  else if constexpr (EPI == EPI_CHEB1) return q == 0 ? A.x : (q == 1 ? A.r : A.invd);
+  else if constexpr (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) return q == 0 ? A.b : A.invd;
+  else if constexpr (EPI == EPI_RESID) return A.b;
+  else return A.y;
+}
 
-// epilogue with prefetched interior operands (slot-local index sl within element e)
-template <int EPI, int NO, int EPB>
-__device__ __forceinline__ void epilogue_pf(const SemArgs& A, long slot, int le, int sl, double w, double dv,
-                                            const double* so) {
-  const double* o0 = so + (std::size_t)le * NO;
-  const double* o1 = so + (std::size_t)(EPB + le) * NO;
-  const double* o2 = so + (std::size_t)(2 * EPB + le) * NO;
+// o0..o2: the operands at this slot (prefetched or loaded); w = (A u) at the node
+template <int EPI>
+__device__ __forceinline__ void epilogue(const SemArgs& A, long slot, double w, double dv, double o0,
+                                         double o1, double o2) {
   if constexpr (EPI == EPI_STORE) {
     A.y[slot] = w;
   } else if constexpr (EPI == EPI_ADD) {
-    A.y[slot] = o0[sl] + w;
+    A.y[slot] = o0 + w;
   } else if constexpr (EPI == EPI_RESID) {
-    A.r[slot] = o0[sl] - w;
-  } else if constexpr (EPI == EPI_CHEB4) {  // o0 = x, o1 = r_in, o2 = invd
-    A.x[slot] = A.x_zero ? A.beta * dv : o0[sl] + A.beta * dv;
-    const double rv = o1[sl] - w;
+    A.r[slot] = o0 - w;
+  } else if constexpr (EPI == EPI_CHEB4) {
+    // smoothers.hpp:138-144: x += beta d ; r -= A d ; d = c1 d + c2 invD r
+    A.x[slot] = A.x_zero ? A.beta * dv : o0 + A.beta * dv;
+    const double rv = o1 - w;
     A.r[slot] = rv;
-    A.d_out[slot] = A.c1 * dv + A.c2 * o2[sl] * rv;
-  } else if constexpr (EPI == EPI_CHEB1) {  // o0 = x, o1 = z, o2 = invd
-    A.x[slot] = A.x_zero ? dv : o0[sl] + dv;
-    const double zv = o1[sl] - o2[sl] * w;
+    A.d_out[slot] = A.c1 * dv + A.c2 * o2 * rv;
+  } else if constexpr (EPI == EPI_CHEB1) {
+    // smoothers.hpp:109-118: x += d ; z -= invD A d ; d = c1 d + c2 z
+    A.x[slot] = A.x_zero ? dv : o0 + dv;
+    const double zv = o1 - o2 * w;
     A.r[slot] = zv;
     A.d_out[slot] = A.c1 * dv + A.c2 * zv;
-  } else if constexpr (EPI == EPI_CHEB4_INIT) {  // o0 = b, o1 = invd
-    const double rv = o0[sl] - w;
+  } else if constexpr (EPI == EPI_CHEB4_INIT) {
+    const double rv = o0 - w;
     A.r[slot] = rv;
-    A.d_out[slot] = A.c0 * o1[sl] * rv;
+    A.d_out[slot] = A.c0 * o1 * rv;
   } else if constexpr (EPI == EPI_CHEB1_INIT) {
-    const double zv = (o0[sl] - w) * o1[sl];
+    const double zv = (o0 - w) * o1;
     A.r[slot] = zv;
     A.d_out[slot] = zv / A.theta;
   }
 }
 
+// ---------------------------------------------------------------- K1 (AX mode)
 template <int N, int EPI>
-__global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_tma(SemArgs A) {
+struct K1Smem {
+  using C = SemC<N>;
+  static constexpr int NOPS = EpiOps<EPI>::n;
+  static constexpr std::size_t g_off = 0;                                            // [EPB][6][NP]
+  static constexpr std::size_t u_off = g_off + (std::size_t)C::EPB * 6 * C::NP;      // [EPB][NP]
+  static constexpr std::size_t o_off = u_off + (((std::size_t)C::EPB * C::NP + 1) & ~(std::size_t)1);  // [EPB][NOPS][NINT_PAD], 16B-aligned
+  static constexpr std::size_t d_off = o_off + (std::size_t)C::EPB * NOPS * C::NINT_PAD;  // [N1][N1+1]
+  static constexpr std::size_t bar_off = d_off + (std::size_t)C::N1 * (C::N1 + 1);
+  static constexpr std::size_t bytes = (bar_off + 1) * sizeof(double);
+};
+
+template <int N, int EPI>
+__global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
   using C = SemC<N>;
   using S = K1Smem<N, EPI>;
-  constexpr int N1 = C::N1, NP = C::NP, NO = C::NO, TPE = C::TPE, EPB = C::EPB;
+  constexpr int N1 = C::N1, NP = C::NP, NOS = C::NOS, TPE = C::TPE, EPB = C::EPB, KN = C::KN;
+  constexpr int NOPS = S::NOPS, NIP = C::NINT_PAD;
   extern __shared__ __align__(128) double sm[];
   double* sG = sm + S::g_off;
   double* su = sm + S::u_off;
@@ -274,72 +155,65 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_tma(SemArgs A) {
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
   const int le = threadIdx.x / TPE;
   const int t = threadIdx.x - le * TPE;
-  const int i = t % N1, j = t / N1;
+  const int i = t % N1, j = (t / N1) % N1, kh = t / (N1 * N1);
+  const int kb = kh * KN;
   const long e0 = A.e_begin + (long)blockIdx.x * EPB;
   const long e = e0 + le;
   const bool active = e < A.e_end;
   const int nact = (int)min((long)EPB, A.e_end - e0);
-  // 1. one thread streams the block's geometric factors (EPB x 24.6 KB at N=7) with TMA
+  // 1. one thread streams geometric factors + interior operand blocks with TMA
   if (threadIdx.x == 0) {
+    const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
+    unsigned bytes = (unsigned)(nact * 6 * NP * sizeof(double));
+    if constexpr (NOPS > 0 && C::NINT > 0) bytes += (unsigned)(nact * (NOPS - (skip_x ? 1 : 0)) * NIP * 8);
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, (unsigned)(nact * 6 * NP * sizeof(double)));
-    for (int q = 0; q < nact; ++q)
+    mbar_expect_tx(bar, bytes);
+    for (int q = 0; q < nact; ++q) {
       bulk_g2s(sG + (std::size_t)q * 6 * NP, A.G + (e0 + q) * 6 * NP, 6 * NP * sizeof(double), bar);
+      if constexpr (NOPS > 0 && C::NINT > 0) {
+#pragma unroll
+        for (int op = 0; op < NOPS; ++op) {
+          if (op == 0 && skip_x) continue;
+          bulk_g2s(so + ((std::size_t)q * NOPS + op) * NIP, epi_op<EPI>(A, op) + (e0 + q) * NOS, NIP * 8, bar);
+        }
+      }
+    }
   }
   for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) sD[q / N1][q % N1] = A.D[q];
   const int ex = active ? (int)(e % A.Ex) : 0;
   const int ey = active ? (int)((e / A.Ex) % A.Ey) : 0;
   const int ez = active ? (int)(e / ((long)A.Ex * A.Ey)) : 0;
-  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
-  // 2. async prefetch of the epilogue operands of this thread's interior column
-  if constexpr (S::NOPS > 0) {
-    if (active && ij_interior) {
-      const double* ops[3];
-      if constexpr (EPI == EPI_CHEB4) { ops[0] = A.x; ops[1] = A.r_in; ops[2] = A.invd; }
-      else if constexpr (EPI == EPI_CHEB1) { ops[0] = A.x; ops[1] = A.r; ops[2] = A.invd; }
-      else if constexpr (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) { ops[0] = A.b; ops[1] = A.invd; ops[2] = nullptr; }
-      else if constexpr (EPI == EPI_RESID) { ops[0] = A.b; ops[1] = nullptr; ops[2] = nullptr; }
-      else { ops[0] = A.y; ops[1] = nullptr; ops[2] = nullptr; }
-#pragma unroll
-      for (int q = 0; q < S::NOPS; ++q) {
-        if (q == 0 && (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero) continue;  // x not read
-#pragma unroll
-        for (int k = 1; k < N; ++k) {
-          const int sl = (i - 1) + N * ((j - 1) + N * (k - 1));
-          cp_async8(so + ((std::size_t)q * EPB + le) * NO + sl, ops[q] + e * NO + sl);
-        }
-      }
-    }
-  }
-  // 3. gather Q u (owner slots / halo / Dirichlet zero) into shared memory
+  // 2. gather Q u (owner slots / halo / Dirichlet zero) into shared memory
+  double* ue = su + (std::size_t)le * NP;
   {
-    int oex, oey;
+    int oex = 0, oey = 0;
     const int ax = owner1d<N>(ex, i, A.Ex, oex);
     const int ay = owner1d<N>(ey, j, A.Ey, oey);
 #pragma unroll
-    for (int k = 0; k < N1; ++k) {
+    for (int kk = 0; kk < KN; ++kk) {
+      const int k = kb + kk;
       double v = 0.0;
       if (active && ax >= 0 && ay >= 0) {
-        int oez;
+        int oez = 0;
         const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
         if (az >= 0) {
           const int lz = oez - A.z0;
           if (lz < 0)
             v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
           else
-            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NO + ax + N * (ay + N * az)];
+            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS + sem_pos(N, ax, ay, az)];
         }
       }
-      su[(std::size_t)le * NP + (k * N1 + j) * N1 + i] = v;
+      ue[(k * N1 + j) * N1 + i] = v;
     }
   }
   __syncthreads();
   mbar_wait(bar, 0);
-  // 4. gradient + geometric factors; w_r, w_s, w_t overwrite G_rr, G_rs, G_rt in place
+  // 3. gradient + geometric factors: w_r, w_s, w_t overwrite G_rr, G_rs, G_rt in place
   double* Ge = sG + (std::size_t)le * 6 * NP;
-  const double* ue = su + (std::size_t)le * NP;
 #pragma unroll
-  for (int k = 0; k < N1; ++k) {
+  for (int kk = 0; kk < KN; ++kk) {
+    const int k = kb + kk;
     const int l = (k * N1 + j) * N1 + i;
     double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
@@ -356,10 +230,12 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_tma(SemArgs A) {
   }
   __syncthreads();
   if (!active) return;
-  if constexpr (S::NOPS > 0) cp_async_wait_all();
-  // 5. divergence + epilogue
+  // 4. divergence + epilogue (interior nodes finished, shell nodes to the shell buffer)
+  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+  const double* soe = so + (std::size_t)le * NOPS * NIP;
 #pragma unroll
-  for (int k = 0; k < N1; ++k) {
+  for (int kk = 0; kk < KN; ++kk) {
+    const int k = kb + kk;
     double v = 0.0;
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
@@ -368,27 +244,52 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_tma(SemArgs A) {
       v += sD[m][k] * Ge[2 * NP + (m * N1 + j) * N1 + i];
     }
     if (ij_interior && k >= 1 && k < N) {
-      const int sl = (i - 1) + N * ((j - 1) + N * (k - 1));
+      const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
       const double dv = ue[(k * N1 + j) * N1 + i];
-      epilogue_pf<EPI, NO, EPB>(A, e * NO + sl, le, sl, v, dv, so);
+      double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+      if constexpr (NOPS > 0) o0 = soe[p];
+      if constexpr (NOPS > 1) o1 = soe[NIP + p];
+      if constexpr (NOPS > 2) o2 = soe[2 * NIP + p];
+      epilogue<EPI>(A, e * NOS + p, v, dv, o0, o1, o2);
     } else {
       A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
     }
   }
 }
 
+// ---------------------------------------------------------------- K1 (LVEC mode: assemble an L-vector)
+template <int N, int EPI>
+__global__ void k_sem_k1_lvec(SemArgs A) {
+  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N);
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long e = A.e_begin + t / NP;
+  if (e >= A.e_end) return;
+  const int l = (int)(t % NP);
+  const int i = l % N1, j = (l / N1) % N1, k = l / (N1 * N1);
+  const double v = A.lvec[e * NP + l];
+  if (i >= 1 && i < N && j >= 1 && j < N && k >= 1 && k < N) {
+    const long slot = e * NOS + (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
+    double o0 = 0.0, o1 = 0.0;
+    if constexpr (EpiOps<EPI>::n > 0) o0 = epi_op<EPI>(A, 0)[slot];
+    if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
+    epilogue<EPI>(A, slot, v, 0.0, o0, o1, 0.0);
+  } else {
+    A.shell[e * A.nshell + A.lut[l]] = v;
+  }
+}
+
 // ---------------------------------------------------------------- K2
 template <int N, int EPI>
 __global__ void k_sem_k2(SemArgs A) {
-  constexpr int N1 = N + 1, NO = N * N * N;
+  constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N), NSH = sem_nshared(N);
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long q = tid / A.nshared;
-  const int s = (int)(tid - q * A.nshared);
+  const long q = tid / NSH;
+  const int s = (int)(tid - q * NSH);
   const long e = A.e_begin + q;
   if (e >= A.e_end) return;
   const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-  const int sl = A.shared[s];
-  const int a = sl % N, b = (sl / N) % N, c = sl / (N * N);
+  int a, b, c;
+  sem_shared_abc(N, s, a, b, c);
   // padding (far domain boundary) is not an unknown
   if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
   const int i = a + 1, j = b + 1, k = c + 1;
@@ -407,10 +308,18 @@ __global__ void k_sem_k2(SemArgs A) {
         }
         sum += v;
       }
-  const long slot = e * NO + sl;
-  double dv = 0.0;
-  if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) dv = A.d[slot];
-  epilogue<EPI>(A, slot, sum, dv);
+  const long slot = e * NOS + NINT + s;
+  double dv = 0.0, o0 = 0.0, o1 = 0.0, o2 = 0.0;
+  if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) {
+    dv = A.d[slot];
+    if (!A.x_zero) o0 = A.x[slot];
+    o1 = epi_op<EPI>(A, 1)[slot];
+    o2 = A.invd[slot];
+  } else {
+    if constexpr (EpiOps<EPI>::n > 0) o0 = epi_op<EPI>(A, 0)[slot];
+    if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
+  }
+  epilogue<EPI>(A, slot, sum, dv, o0, o1, o2);
 }
 
 template <int N, int MODE, int EPI>
@@ -418,18 +327,18 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   using C = SemC<N>;
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
-  const long blocks = (ne + C::EPB - 1) / C::EPB;
   if constexpr (MODE == SEM_AX) {
     constexpr std::size_t smem = K1Smem<N, EPI>::bytes;
     static bool configured = false;
     if (!configured) {
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_tma<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_ax<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       configured = true;
     }
-    k_sem_k1_tma<N, EPI><<<(unsigned)blocks, C::NT, smem, s>>>(a);
+    const long blocks = (ne + C::EPB - 1) / C::EPB;
+    k_sem_k1_ax<N, EPI><<<(unsigned)blocks, C::NT, smem, s>>>(a);
   } else {
-    k_sem_k1<N, MODE, EPI><<<(unsigned)blocks, C::NT, 0, s>>>(a);
+    const long threads = ne * C::NP;
+    k_sem_k1_lvec<N, EPI><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
   }
   CMG_LAUNCH_CHECK();
 }
@@ -437,8 +346,8 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
 template <int N, int EPI>
 void launch_k2(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
-  if (ne <= 0 || a.nshared == 0) return;
-  const long threads = ne * a.nshared;
+  if (ne <= 0) return;
+  const long threads = ne * sem_nshared(N);
   k_sem_k2<N, EPI><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
   CMG_LAUNCH_CHECK();
 }
@@ -460,7 +369,9 @@ void dispatch_k1_epi(const SemArgs& a, int epi, cudaStream_t s) {
 template <int N>
 void dispatch_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
   if (mode == SEM_AX) dispatch_k1_epi<N, SEM_AX>(a, epi, s);
-  else dispatch_k1_epi<N, SEM_LVEC>(a, epi, s);
+  else if (epi == EPI_STORE) launch_k1<N, SEM_LVEC, EPI_STORE>(a, s);
+  else if (epi == EPI_ADD) launch_k1<N, SEM_LVEC, EPI_ADD>(a, s);
+  else throw Error(EINVAL_, "sem_k1: LVEC mode supports STORE/ADD");
 }
 
 template <int N>
@@ -515,7 +426,8 @@ __global__ void k_pack_top(SemArgs A, const double* __restrict__ u, double* __re
   const int ab = (int)(t % (N * N));
   const long exy = t / (N * N);
   const long e = exy + (long)A.Ex * A.Ey * (A.Ezl - 1);
-  buf[t] = u[e * N * N * N + ab + (long)N * N * (N - 1)];
+  // the c = N-1 plane: last N^2 shared slots, (b, a) lexicographic
+  buf[t] = u[e * sem_nos(N) + sem_nint(N) + (N - 1) * (2 * N - 1) + ab];
 }
 
 __global__ void k_pack_contrib_bottom(SemArgs A, double* __restrict__ buf) {
@@ -565,11 +477,11 @@ __device__ void kershaw(double eps, double x, double y, double z, double& X, dou
 // one block per element, one thread per node
 __global__ void k_geometry(SemGeom g, double* __restrict__ G, double* __restrict__ Lrhs,
                            double* __restrict__ Lmass) {
-  extern __shared__ double sm[];
+  extern __shared__ double smg[];
   const int N = g.N, N1 = N + 1, NP = N1 * N1 * N1;
-  double* X = sm;
-  double* Y = sm + NP;
-  double* Z = sm + 2 * NP;
+  double* X = smg;
+  double* Y = smg + NP;
+  double* Z = smg + 2 * NP;
   const long e = blockIdx.x;
   const int ex = (int)(e % g.Ex), ey = (int)((e / g.Ex) % g.Ey), ez = g.z0 + (int)(e / ((long)g.Ex * g.Ey));
   for (int l = threadIdx.x; l < NP; l += blockDim.x) {
@@ -648,17 +560,17 @@ __global__ void k_local_diag(int N, const double* __restrict__ G, const double* 
 
 __device__ __forceinline__ bool slot_valid(const SemArgs& A, long q) {
   const int N = A.N;
-  const long NO = (long)N * N * N;
-  const long e = q / NO;
-  const int sl = (int)(q - e * NO);
-  const int a = sl % N, b = (sl / N) % N, c = sl / (N * N);
+  const long NOS = sem_nos(N);
+  const long e = q / NOS;
+  int a, b, c;
+  if (!sem_abc(N, (int)(q - e * NOS), a, b, c)) return false;
   const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
   return ex * N + a + 1 < N * A.Ex && ey * N + b + 1 < N * A.Ey && (A.z0 + ez) * N + c + 1 < N * A.Ez;
 }
 
 __global__ void k_inverse_diag(SemArgs A, const double* __restrict__ d, double* __restrict__ inv,
                                int* zero_flag) {
-  const long n = A.E * (long)A.N * A.N * A.N;
+  const long n = A.E * (long)sem_nos(A.N);
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) {
     if (slot_valid(A, q)) {
       const double v = d[q];
@@ -671,13 +583,13 @@ __global__ void k_inverse_diag(SemArgs A, const double* __restrict__ d, double* 
 }
 
 __global__ void k_flag_zero_valid(SemArgs A, const double* __restrict__ v, int* flag) {
-  const long n = A.E * (long)A.N * A.N * A.N;
+  const long n = A.E * (long)sem_nos(A.N);
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x)
     if (v[q] == 0.0 && slot_valid(A, q)) atomicExch(flag, 1);
 }
 
 __global__ void k_slot_mask(SemArgs A, double* __restrict__ m) {
-  const long n = A.E * (long)A.N * A.N * A.N;
+  const long n = A.E * (long)sem_nos(A.N);
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x)
     m[q] = slot_valid(A, q) ? 1.0 : 0.0;
 }
@@ -687,7 +599,8 @@ __global__ void k_slot_mask(SemArgs A, double* __restrict__ m) {
 template <int NF, int NCO>
 __global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
                           const double* __restrict__ xc, double* __restrict__ yf, int add) {
-  constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF, NOC = NCO * NCO * NCO;
+  constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF;
+  constexpr int NOSF = sem_nos(NF), NOSC = sem_nos(NCO);
   __shared__ double sJ[F1 * C1];
   __shared__ double uc[C1 * C1 * C1];
   __shared__ double t1[F1 * C1 * C1];
@@ -697,7 +610,7 @@ __global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
   for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
   for (int q = threadIdx.x; q < C1 * C1 * C1; q += blockDim.x) {
     const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
-    int oex, oey, oez;
+    int oex = 0, oey = 0, oez = 0;
     const int ax = owner1d<NCO>(ex, a, Cc.Ex, oex);
     const int ay = owner1d<NCO>(ey, b, Cc.Ey, oey);
     const int az = owner1d<NCO>(Cc.z0 + ez, c, Cc.Ez, oez);
@@ -707,7 +620,7 @@ __global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
       if (lz < 0)
         v = Cc.halo_lo[((long)oex + (long)Cc.Ex * oey) * (NCO * NCO) + ax + NCO * ay];
       else
-        v = xc[((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOC + ax + NCO * (ay + NCO * az)];
+        v = xc[((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOSC + sem_pos(NCO, ax, ay, az)];
     }
     uc[q] = v;
   }
@@ -732,7 +645,7 @@ __global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
     if (ex * NF + i >= NF * F.Ex || ey * NF + j >= NF * F.Ey || (F.z0 + ez) * NF + k >= NF * F.Ez) continue;
     double v = 0.0;
     for (int m = 0; m < C1; ++m) v += sJ[k * C1 + m] * t2[i + F1 * (j + F1 * m)];
-    const long slot = e * NOF + q;
+    const long slot = e * NOSF + sem_pos(NF, a, b, c);
     yf[slot] = add ? yf[slot] + v : v;
   }
 }
@@ -740,7 +653,7 @@ __global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
 template <int NF, int NCO>
 __global__ void k_restrict_local(SemArgs F, const double* __restrict__ J, const double* __restrict__ xf,
                                  double* __restrict__ Lc) {
-  constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF, CP = C1 * C1 * C1;
+  constexpr int F1 = NF + 1, C1 = NCO + 1, CP = C1 * C1 * C1, NOSF = sem_nos(NF);
   __shared__ double sJ[F1 * C1];
   __shared__ double uf[F1 * F1 * F1];
   __shared__ double t1[C1 * F1 * F1];
@@ -750,7 +663,7 @@ __global__ void k_restrict_local(SemArgs F, const double* __restrict__ J, const 
   for (int q = threadIdx.x; q < F1 * F1 * F1; q += blockDim.x) {
     const int i = q % F1, j = (q / F1) % F1, k = q / (F1 * F1);
     double v = 0.0;
-    if (i >= 1 && j >= 1 && k >= 1) v = xf[e * NOF + (i - 1) + NF * ((j - 1) + NF * (k - 1))];
+    if (i >= 1 && j >= 1 && k >= 1) v = xf[e * NOSF + sem_pos(NF, i - 1, j - 1, k - 1)];
     uf[q] = v;  // padding slots are zero
   }
   __syncthreads();
@@ -777,7 +690,7 @@ __global__ void k_restrict_local(SemArgs F, const double* __restrict__ J, const 
 }
 
 // ---------------------------------------------------------------- layer dots
-// partials[(v*L + layer)*CH + chunk]
+// partials[(v*L + layer)*LCH + chunk]
 constexpr int LCH = 16;
 __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int nv,
                              const double* __restrict__ w, long layer_len, int nlayers,
@@ -837,27 +750,19 @@ __global__ void k_layer_finalize(const double* __restrict__ g, int nv, const int
 }  // namespace
 
 // ====================================================================== host launchers
+#define CMG_ORDERS(X) X(1) X(2) X(3) X(4) X(5) X(7)
+
 void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
-  switch (a.N) {
-    case 1: return dispatch_k1<1>(a, mode, epi, s);
-    case 2: return dispatch_k1<2>(a, mode, epi, s);
-    case 3: return dispatch_k1<3>(a, mode, epi, s);
-    case 4: return dispatch_k1<4>(a, mode, epi, s);
-    case 5: return dispatch_k1<5>(a, mode, epi, s);
-    case 7: return dispatch_k1<7>(a, mode, epi, s);
-  }
+#define X(n) if (a.N == n) return dispatch_k1<n>(a, mode, epi, s);
+  CMG_ORDERS(X)
+#undef X
   throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
 }
 
 void sem_k2(const SemArgs& a, int epi, cudaStream_t s) {
-  switch (a.N) {
-    case 1: return dispatch_k2<1>(a, epi, s);
-    case 2: return dispatch_k2<2>(a, epi, s);
-    case 3: return dispatch_k2<3>(a, epi, s);
-    case 4: return dispatch_k2<4>(a, epi, s);
-    case 5: return dispatch_k2<5>(a, epi, s);
-    case 7: return dispatch_k2<7>(a, epi, s);
-  }
+#define X(n) if (a.N == n) return dispatch_k2<n>(a, epi, s);
+  CMG_ORDERS(X)
+#undef X
   throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
 }
 
@@ -899,19 +804,19 @@ void sem_local_diag(int N, long E, const double* G, const double* D, double* Ldi
 
 void sem_inverse_diag(const SemArgs& a, const double* diag, double* invd, int* zero_flag,
                       cudaStream_t s) {
-  const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
+  const std::size_t n = (std::size_t)a.E * sem_nos(a.N);
   k_inverse_diag<<<vgrid(n), 256, 0, s>>>(a, diag, invd, zero_flag);
   CMG_LAUNCH_CHECK();
 }
 
 void sem_flag_zero_valid(const SemArgs& a, const double* v, int* flag, cudaStream_t s) {
-  const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
+  const std::size_t n = (std::size_t)a.E * sem_nos(a.N);
   k_flag_zero_valid<<<vgrid(n), 256, 0, s>>>(a, v, flag);
   CMG_LAUNCH_CHECK();
 }
 
 void sem_slot_mask(const SemArgs& a, double* mask, cudaStream_t s) {
-  const std::size_t n = (std::size_t)a.E * a.N * a.N * a.N;
+  const std::size_t n = (std::size_t)a.E * sem_nos(a.N);
   k_slot_mask<<<vgrid(n), 256, 0, s>>>(a, mask);
   CMG_LAUNCH_CHECK();
 }

@@ -18,6 +18,7 @@
 
 #include "cmg_objects.hpp"
 #include "sem_kernels.hpp"
+#include "sem_layout.hpp"
 
 using namespace cmg;
 
@@ -69,10 +70,10 @@ void partition(const cmg_sem_desc& d, int& z0, int& z1) {
 
 long canonical_of_slot(const cmg_sem_desc& d, int z0, long q) {
   const int N = d.order;
-  const long NO = static_cast<long>(N) * N * N;
-  const long e = q / NO;
-  const int sl = static_cast<int>(q - e * NO);
-  const int a = sl % N, b = (sl / N) % N, c = sl / (N * N);
+  const long NOS = sem_nos(N);
+  const long e = q / NOS;
+  int a, b, c;
+  if (!sem_abc(N, static_cast<int>(q - e * NOS), a, b, c)) return -1;  // pad slot
   const int ex = static_cast<int>(e % d.ex), ey = static_cast<int>((e / d.ex) % d.ey);
   const int ez = z0 + static_cast<int>(e / (static_cast<long>(d.ex) * d.ey));
   const long gx = static_cast<long>(ex) * N + a + 1, gy = static_cast<long>(ey) * N + b + 1,
@@ -112,8 +113,7 @@ struct SemLevel final : cmg_op {
         fail(CMG_EINVAL, "sem: context has no matching NCCL communicator (cmg_ctx_attach_nccl)");
     }
     E = static_cast<long>(Ex) * Ey * Ezl;
-    const long NO = static_cast<long>(N) * N * N;
-    len = static_cast<std::size_t>(E * NO);
+    len = static_cast<std::size_t>(E * sem_nos(N));
     n = static_cast<std::size_t>((static_cast<long>(N) * Ex - 1) * (static_cast<long>(N) * Ey - 1) *
                                  (static_cast<long>(N) * Ez - 1));
     const int N1 = N + 1, NP = N1 * N1 * N1;
@@ -326,7 +326,7 @@ struct SemLevel final : cmg_op {
   void layer_reduce(const double* V, std::size_t ldv, int nv, const double* w, double* out,
                     bool do_sqrt) {
     if (nv > 64) fail(CMG_EINVAL, "sem: too many vectors in one reduction");
-    const long layer_len = static_cast<long>(Ex) * Ey * N * N * N;
+    const long layer_len = static_cast<long>(Ex) * Ey * sem_nos(N);
     sem_layer_dots(V, ldv, nv, w, layer_len, Ezl, lpart.p, lout.p, ctx->stream);
     const double* g = lout.p;
     if (distributed()) {
@@ -410,32 +410,32 @@ void pmg_fdm_box(cmg_pmg* p, const double* rc, double* ec) {
   SemLevel* c = p->lev.back().get();
   cudaStream_t s = p->ctx->stream;
   if (c->N != 1) fail(CMG_EINVAL, "pmg: the coarsest level must be p=1");
-  const long full = static_cast<long>(c->Ex) * c->Ey * c->Ez;
+  const long full = static_cast<long>(c->Ex) * c->Ey * c->Ez * sem_nos(1);
   const double* in = rc;
   if (c->distributed()) {
     p->ctx->comm->allgather(rc, p->cfull.p, c->len, s);
     in = p->cfull.p;
   }
   const int nx = p->cnx, ny = p->cny, nz = p->cnz;
-  const long s1 = c->Ex, s2 = static_cast<long>(c->Ex) * c->Ey;
+  const long s0 = sem_nos(1), s1 = s0 * c->Ex, s2 = s1 * c->Ey;
   if (nx < 1 || ny < 1 || nz < 1) {  // no interior p=1 unknowns
     CMG_CUDA(cudaMemsetAsync(ec, 0, c->len * sizeof(double), s));
     return;
   }
   CMG_CUDA(cudaMemsetAsync(p->t1.p, 0, full * sizeof(double), s));
   CMG_CUDA(cudaMemsetAsync(p->t2.p, 0, full * sizeof(double), s));
-  mode_product(0, nx, ny, nz, s1, s2, p->Sx.p, nx, true, in, p->t1.p, nullptr, s);
-  mode_product(1, nx, ny, nz, s1, s2, p->Sy.p, ny, true, p->t1.p, p->t2.p, nullptr, s);
-  mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, true, p->t2.p, p->t1.p, p->Dg.p, s);
-  mode_product(0, nx, ny, nz, s1, s2, p->Sx.p, nx, false, p->t1.p, p->t2.p, nullptr, s);
-  mode_product(1, nx, ny, nz, s1, s2, p->Sy.p, ny, false, p->t2.p, p->t1.p, nullptr, s);
+  mode_product_s0(0, nx, ny, nz, s0, s1, s2, p->Sx.p, nx, true, in, p->t1.p, nullptr, s);
+  mode_product_s0(1, nx, ny, nz, s0, s1, s2, p->Sy.p, ny, true, p->t1.p, p->t2.p, nullptr, s);
+  mode_product_s0(2, nx, ny, nz, s0, s1, s2, p->Sz.p, nz, true, p->t2.p, p->t1.p, p->Dg.p, s);
+  mode_product_s0(0, nx, ny, nz, s0, s1, s2, p->Sx.p, nx, false, p->t1.p, p->t2.p, nullptr, s);
+  mode_product_s0(1, nx, ny, nz, s0, s1, s2, p->Sy.p, ny, false, p->t2.p, p->t1.p, nullptr, s);
   if (c->distributed()) {
-    mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, false, p->t1.p, p->t2.p, nullptr, s);
+    mode_product_s0(2, nx, ny, nz, s0, s1, s2, p->Sz.p, nz, false, p->t1.p, p->t2.p, nullptr, s);
     CMG_CUDA(cudaMemcpyAsync(ec, p->t2.p + static_cast<long>(c->z0) * s2, c->len * sizeof(double),
                              cudaMemcpyDeviceToDevice, s));
   } else {
     CMG_CUDA(cudaMemsetAsync(ec, 0, c->len * sizeof(double), s));
-    mode_product(2, nx, ny, nz, s1, s2, p->Sz.p, nz, false, p->t1.p, ec, nullptr, s);
+    mode_product_s0(2, nx, ny, nz, s0, s1, s2, p->Sz.p, nz, false, p->t1.p, ec, nullptr, s);
   }
 }
 
@@ -566,7 +566,7 @@ int cmg_sem_partition(const cmg_sem_desc* d, int* z0, int* z1) {
 size_t cmg_sem_local_slots(const cmg_sem_desc* d) {
   int z0, z1;
   partition(*d, z0, z1);
-  return static_cast<size_t>(d->ex) * d->ey * (z1 - z0) * d->order * d->order * d->order;
+  return static_cast<size_t>(d->ex) * d->ey * (z1 - z0) * sem_nos(d->order);
 }
 
 int cmg_sem_slot_map_host(const cmg_sem_desc* d, int64_t* map) {
@@ -675,12 +675,12 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
     p->cnx = C->Ex - 1;
     p->cny = C->Ey - 1;
     p->cnz = C->Ez - 1;
-    const long full = static_cast<long>(C->Ex) * C->Ey * C->Ez;
+    const long full = static_cast<long>(C->Ex) * C->Ey * C->Ez * sem_nos(1);
     std::vector<double> Dh(full, 1.0);
     for (int k = 0; k < p->cnz; ++k)
       for (int j = 0; j < p->cny; ++j)
         for (int i = 0; i < p->cnx; ++i)
-          Dh[i + static_cast<long>(C->Ex) * (j + static_cast<long>(C->Ey) * k)] = lx[i] + ly[j] + lz[k];
+          Dh[sem_nos(1) * (i + static_cast<long>(C->Ex) * (j + static_cast<long>(C->Ey) * k))] = lx[i] + ly[j] + lz[k];
     p->Dg.alloc(full);
     CMG_CUDA(cudaMemcpy(p->Dg.p, Dh.data(), full * sizeof(double), cudaMemcpyHostToDevice));
     p->cfull.alloc(full);

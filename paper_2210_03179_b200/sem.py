@@ -61,6 +61,23 @@ class SemDesc:
         return z0.value, z1.value
 
 
+def slots_per_element(N: int) -> int:
+    """csrc/sem_layout.hpp sem_nos: N^3 owned slots padded to an even count."""
+    return (N * N * N + 1) & ~1
+
+
+def slot_pos(N: int, a: int, b: int, c: int) -> int:
+    """csrc/sem_layout.hpp sem_pos: interior-first element-local slot of owned node (a,b,c)."""
+    if a < N - 1 and b < N - 1 and c < N - 1:
+        return a + (N - 1) * (b + (N - 1) * c)
+    base = (N - 1) ** 3
+    if c == N - 1:
+        return base + (N - 1) * (2 * N - 1) + b * N + a
+    if b == N - 1:
+        return base + c * (2 * N - 1) + (N - 1) + a
+    return base + c * (2 * N - 1) + b
+
+
 def slot_map(desc: SemDesc) -> np.ndarray:
     """Canonical interior index of every owned slot of this rank (-1 = padding)."""
     m = np.empty(desc.local_slots(), dtype=np.int64)

@@ -65,7 +65,7 @@ def _worker(rank, world, port, q):
                 e = ex + EX * (ey + EY * (Lz - 1))
                 for b in range(N):
                     for a in range(N):
-                        send.append(smap[e * N ** 3 + a + N * (b + N * (N - 1))])
+                        send.append(smap[e * sem.slots_per_element(N) + sem.slot_pos(N, a, b, N - 1)])
         send = torch.tensor(send, dtype=torch.int64)
         recv = torch.empty_like(send)
         ops = []
@@ -101,7 +101,8 @@ def _worker(rank, world, port, q):
             lower = sem.SemDesc(N, EX, EY, EZ, rank=rank - 1, nranks=world)
             lm = sem.slot_map(lower)
             lz0, lz1 = lower.partition()
-            top_ids = set(lm[(EX * EY * (lz1 - lz0 - 1)) * N ** 3:][lm[(EX * EY * (lz1 - lz0 - 1)) * N ** 3:] >= 0])
+            top = lm[(EX * EY * (lz1 - lz0 - 1)) * sem.slots_per_element(N):]
+            top_ids = set(top[top >= 0])
             for ey in range(EY):
                 for ex in range(EX):
                     for j in range(N + 1):
