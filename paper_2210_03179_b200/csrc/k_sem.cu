@@ -257,6 +257,187 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
   }
 }
 
+// ---------------------------------------------------------------- K1 v3 (AX mode, register-blocked)
+// GLL derivative matrices per order in constant memory: with compile-time
+// indices every D entry becomes a DFMA constant-bank operand (no LDS).
+__constant__ double c_D[8][64];
+
+// Line-blocked layout: one block = one element, (N+1)^2 threads.  Each
+// contraction is done by a thread owning a whole line of N+1 nodes along the
+// contracted direction: N+1 shared loads, (N+1)^2 DFMAs with constant D,
+// N+1 stores -- one shared access per output instead of 2(N+1).  Rows are
+// padded to N+2 doubles (conflict-free line loads).
+template <int N, int EPI>
+struct K3Smem {
+  static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NPP = N1 * N1 * (N1 + 1);
+  static constexpr int NOPS = EpiOps<EPI>::n, NIP = SemC<N>::NINT_PAD;
+  static constexpr std::size_t g_off = 0;                                  // [6][NP]  (TMA)
+  static constexpr std::size_t o_off = g_off + (std::size_t)6 * NP;        // [NOPS][NIP] (TMA)
+  static constexpr std::size_t u_off = o_off + (std::size_t)NOPS * NIP;    // [NPP] u, later v
+  static constexpr std::size_t r_off = u_off + NPP;                        // [NPP] u_r -> w_r
+  static constexpr std::size_t s_off = r_off + NPP;                        // [NPP] u_s -> w_s
+  static constexpr std::size_t bar_off = (s_off + NPP + 1) & ~(std::size_t)1;
+  static constexpr std::size_t bytes = (bar_off + 1) * sizeof(double);
+};
+
+template <int N, int EPI>
+__global__ void __launch_bounds__((N + 1) * (N + 1)) k_sem_k1_v3(SemArgs A) {
+  using S = K3Smem<N, EPI>;
+  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
+  constexpr int R = N1 + 1;  // padded row length
+#define IDX(i, j, k) (((k) * N1 + (j)) * R + (i))
+#define CD(a, b) c_D[N][(a) * N1 + (b)]
+  extern __shared__ __align__(128) double sm[];
+  double* sG = sm + S::g_off;
+  double* so = sm + S::o_off;
+  double* su = sm + S::u_off;
+  double* sr = sm + S::r_off;
+  double* ss = sm + S::s_off;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
+  const int t = threadIdx.x;
+  const int ta = t % N1, tb = t / N1;  // line coordinates
+  const long e = A.e_begin + blockIdx.x;
+  // 1. TMA: geometric factors + interior operand blocks
+  if (t == 0) {
+    const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
+    unsigned bytes = 6 * NP * sizeof(double);
+    if constexpr (NOPS > 0 && sem_nint(N) > 0) bytes += (NOPS - (skip_x ? 1 : 0)) * NIP * 8;
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(sG, A.G + e * 6 * NP, 6 * NP * sizeof(double), bar);
+    if constexpr (NOPS > 0 && sem_nint(N) > 0) {
+#pragma unroll
+      for (int op = 0; op < NOPS; ++op) {
+        if (op == 0 && skip_x) continue;
+        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * NOS, NIP * 8, bar);
+      }
+    }
+  }
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  // 2. gather: thread (i,j) = (ta,tb) owns the k-column; keep it in registers too
+  double uc[N1];
+  {
+    const int i = ta, j = tb;
+    int oex = 0, oey = 0;
+    const int ax = owner1d<N>(ex, i, A.Ex, oex);
+    const int ay = owner1d<N>(ey, j, A.Ey, oey);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      double v = 0.0;
+      if (ax >= 0 && ay >= 0) {
+        int oez = 0;
+        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
+        if (az >= 0) {
+          const int lz = oez - A.z0;
+          if (lz < 0)
+            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
+          else
+            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS + sem_pos(N, ax, ay, az)];
+        }
+      }
+      uc[k] = v;
+      su[IDX(i, j, k)] = v;
+    }
+  }
+  __syncthreads();
+  // 3. gradient: u_r along rows (j,k)=(ta,tb); u_s along columns (i,k)=(ta,tb); u_t in registers
+  {
+    double l[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = su[IDX(m, ta, tb)];
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(i, m) * l[m];
+      sr[IDX(i, ta, tb)] = v;
+    }
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, m, tb)];
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(j, m) * l[m];
+      ss[IDX(ta, j, tb)] = v;
+    }
+  }
+  double wt[N1];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v += CD(k, m) * uc[m];
+    wt[k] = v;  // u_t for now
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // 4. geometric factors at the thread's (i,j) column: w = G grad u
+  {
+    const int i = ta, j = tb;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int l = (k * N1 + j) * N1 + i;
+      const double ur = sr[IDX(i, j, k)], us = ss[IDX(i, j, k)], ut = wt[k];
+      const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
+      const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
+      sr[IDX(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
+      ss[IDX(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
+      wt[k] = g2 * ur + g4 * us + g5 * ut;
+    }
+  }
+  __syncthreads();
+  // 5. divergence: D^T along rows into su, then columns accumulate, then k in registers
+  {
+    double l[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = sr[IDX(m, ta, tb)];
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(m, i) * l[m];
+      su[IDX(i, ta, tb)] = v;
+    }
+  }
+  __syncthreads();
+  {
+    double l[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = ss[IDX(ta, m, tb)];
+#pragma unroll
+    for (int j = 0; j < N1; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(m, j) * l[m];
+      su[IDX(ta, j, tb)] += v;
+    }
+  }
+  __syncthreads();
+  // 6. t-divergence + epilogue on the (i,j) column
+  const int i = ta, j = tb;
+  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v += CD(m, k) * wt[m];
+    v += su[IDX(i, j, k)];
+    if (ij_interior && k >= 1 && k < N) {
+      const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
+      double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+      if constexpr (NOPS > 0) o0 = so[p];
+      if constexpr (NOPS > 1) o1 = so[NIP + p];
+      if constexpr (NOPS > 2) o2 = so[2 * NIP + p];
+      epilogue<EPI>(A, e * NOS + p, v, uc[k], o0, o1, o2);
+    } else {
+      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
+    }
+  }
+#undef IDX
+#undef CD
+}
+
 // ---------------------------------------------------------------- K1 (LVEC mode: assemble an L-vector)
 template <int N, int EPI>
 __global__ void k_sem_k1_lvec(SemArgs A) {
@@ -327,7 +508,17 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   using C = SemC<N>;
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
-  if constexpr (MODE == SEM_AX) {
+  if constexpr (MODE == SEM_AX && N >= 5) {
+    // register-blocked line kernel: one element per (N+1)^2-thread block
+    constexpr std::size_t smem = K3Smem<N, EPI>::bytes;
+    static bool configured = false;
+    if (!configured) {
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_v3<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = true;
+    }
+    k_sem_k1_v3<N, EPI><<<(unsigned)ne, (N + 1) * (N + 1), smem, s>>>(a);
+  } else if constexpr (MODE == SEM_AX) {
+    // low orders (coarse p-levels): several elements per block, k-split columns
     constexpr std::size_t smem = K1Smem<N, EPI>::bytes;
     static bool configured = false;
     if (!configured) {
@@ -764,6 +955,10 @@ void sem_k2(const SemArgs& a, int epi, cudaStream_t s) {
   CMG_ORDERS(X)
 #undef X
   throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
+}
+
+void sem_set_derivative(int N, const double* D_host) {
+  CMG_CUDA(cudaMemcpyToSymbol(c_D, D_host, (N + 1) * (N + 1) * sizeof(double), (std::size_t)N * 64 * sizeof(double)));
 }
 
 void sem_cheb4_init_zero(std::size_t n, const double* b, const double* invd, double c0, double* r,

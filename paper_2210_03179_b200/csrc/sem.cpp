@@ -143,6 +143,7 @@ struct SemLevel final : cmg_op {
     CMG_CUDA(cudaMemcpy(xi.p, xih.data(), N1 * sizeof(double), cudaMemcpyHostToDevice));
     CMG_CUDA(cudaMemcpy(w.p, wh.data(), N1 * sizeof(double), cudaMemcpyHostToDevice));
     CMG_CUDA(cudaMemcpy(Dm.p, Dh.data(), N1 * N1 * sizeof(double), cudaMemcpyHostToDevice));
+    sem_set_derivative(N, Dh.data());
     cudaStream_t s = ctx->stream;
     // geometry on the device (setup)
     G.alloc(static_cast<std::size_t>(E) * 6 * NP);

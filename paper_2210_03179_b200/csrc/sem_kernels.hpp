@@ -62,6 +62,8 @@ struct SemArgs {
   long e_begin = 0, e_end = 0;
 };
 
+// upload the order-N GLL derivative matrix to constant memory (once per order)
+void sem_set_derivative(int N, const double* D_host);
 // K1 over elements [e_begin, e_end) and K2 over the same elements
 void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s);
 void sem_k2(const SemArgs& a, int epi, cudaStream_t s);
