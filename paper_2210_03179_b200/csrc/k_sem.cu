@@ -648,6 +648,183 @@ __global__ void __launch_bounds__((N + 1) * (N + 1)) k_sem_k1_v4(SemArgs A) {
 #undef CD
 }
 
+// ---------------------------------------------------------------- K1 v5 (line contractions, 2 threads per line)
+// v3's layout (TMA-staged factors/operands, constant-memory D, one shared
+// access per line element) with each line's N+1 outputs split across KS
+// threads: twice the warps of v3 for the same shared memory, ~2 shared loads
+// per output instead of v2's 2(N+1).
+template <int N, int EPI>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_v5(SemArgs A) {
+  using S = K3Smem<N, EPI>;
+  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
+  constexpr int R = N1 + 1;
+  constexpr int KS = 2, KH = N1 / KS;  // outputs per thread per line
+  static_assert(N1 % KS == 0, "v5 needs an even number of GLL points");
+#define IDX(i, j, k) (((k) * N1 + (j)) * R + (i))
+#define CD(a, b) c_D[N][(a) * N1 + (b)]
+  extern __shared__ __align__(128) double sm[];
+  double* sG = sm + S::g_off;
+  double* so = sm + S::o_off;
+  double* su = sm + S::u_off;
+  double* sr = sm + S::r_off;
+  double* ss = sm + S::s_off;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
+  const int t = threadIdx.x;
+  const int line = t % (N1 * N1), h = t / (N1 * N1);
+  const int ta = line % N1, tb = line / N1;
+  const int o0i = h * KH;  // first output index of this thread within a line
+  const long e = A.e_begin + blockIdx.x;
+  if (t == 0) {
+    const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
+    unsigned bytes = 6 * NP * sizeof(double);
+    if constexpr (NOPS > 0 && sem_nint(N) > 0) bytes += (NOPS - (skip_x ? 1 : 0)) * NIP * 8;
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(sG, A.G + e * 6 * NP, 6 * NP * sizeof(double), bar);
+    if constexpr (NOPS > 0 && sem_nint(N) > 0) {
+#pragma unroll
+      for (int op = 0; op < NOPS; ++op) {
+        if (op == 0 && skip_x) continue;
+        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * NOS, NIP * 8, bar);
+      }
+    }
+  }
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  // gather: thread (i,j,h) loads k in [h*KH, h*KH+KH)
+  {
+    const int i = ta, j = tb;
+    int oex = 0, oey = 0;
+    const int ax = owner1d<N>(ex, i, A.Ex, oex);
+    const int ay = owner1d<N>(ey, j, A.Ey, oey);
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk) {
+      const int k = o0i + kk;
+      double v = 0.0;
+      if (ax >= 0 && ay >= 0) {
+        int oez = 0;
+        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
+        if (az >= 0) {
+          const int lz = oez - A.z0;
+          if (lz < 0)
+            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
+          else
+            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS + sem_pos(N, ax, ay, az)];
+        }
+      }
+      su[IDX(i, j, k)] = v;
+    }
+  }
+  __syncthreads();
+  // gradient: r along rows (j,k)=(ta,tb), s along columns (i,k)=(ta,tb), t along (i,j)=(ta,tb)
+  double wt[KH], dvh[KH];
+  {
+    double l[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = su[IDX(m, ta, tb)];
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(o0i + q, m) * l[m];
+      sr[IDX(o0i + q, ta, tb)] = v;
+    }
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, m, tb)];
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(o0i + q, m) * l[m];
+      ss[IDX(ta, o0i + q, tb)] = v;
+    }
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, tb, m)];
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(o0i + q, m) * l[m];
+      wt[q] = v;  // u_t at (ta, tb, o0i+q)
+      dvh[q] = l[o0i + q];
+    }
+  }
+  __syncthreads();
+  mbar_wait(bar, 0);
+  // geometric factors on the (i,j) column, k in this thread's half
+  {
+    const int i = ta, j = tb;
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      const int k = o0i + q;
+      const int l = (k * N1 + j) * N1 + i;
+      const double ur = sr[IDX(i, j, k)], us = ss[IDX(i, j, k)], ut = wt[q];
+      const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
+      const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
+      sr[IDX(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
+      ss[IDX(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
+      wt[q] = g2 * ur + g4 * us + g5 * ut;
+    }
+  }
+  __syncthreads();
+  // divergence r: rows -> su
+  {
+    double l[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = sr[IDX(m, ta, tb)];
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(m, o0i + q) * l[m];
+      su[IDX(o0i + q, ta, tb)] = v;
+    }
+  }
+  __syncthreads();
+  // sr is free: publish w_t so every thread can read whole k-columns
+#pragma unroll
+  for (int q = 0; q < KH; ++q) sr[IDX(ta, tb, o0i + q)] = wt[q];
+  // divergence s: columns accumulate into su (disjoint from the sr writes above)
+  {
+    double l[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) l[m] = ss[IDX(ta, m, tb)];
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) v += CD(m, o0i + q) * l[m];
+      su[IDX(ta, o0i + q, tb)] += v;
+    }
+  }
+  __syncthreads();
+  // divergence t + epilogue on the (i,j) column, k in this thread's half
+  const int i = ta, j = tb;
+  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+  double l[N1];
+#pragma unroll
+  for (int m = 0; m < N1; ++m) l[m] = sr[IDX(i, j, m)];
+#pragma unroll
+  for (int q = 0; q < KH; ++q) {
+    const int k = o0i + q;
+    double v = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) v += CD(m, k) * l[m];
+    v += su[IDX(i, j, k)];
+    if (ij_interior && k >= 1 && k < N) {
+      const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      if constexpr (NOPS > 0) a0 = so[p];
+      if constexpr (NOPS > 1) a1 = so[NIP + p];
+      if constexpr (NOPS > 2) a2 = so[2 * NIP + p];
+      epilogue<EPI>(A, e * NOS + p, v, dvh[q], a0, a1, a2);
+    } else {
+      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
+    }
+  }
+#undef IDX
+#undef CD
+}
+
 // ---------------------------------------------------------------- K1 (LVEC mode: assemble an L-vector)
 template <int N, int EPI>
 __global__ void k_sem_k1_lvec(SemArgs A) {
@@ -718,7 +895,16 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   using C = SemC<N>;
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
-  if constexpr (MODE == SEM_AX && N >= 5) {
+  if constexpr (MODE == SEM_AX && N >= 5 && (N + 1) % 2 == 0) {
+    // line-contraction kernel, two threads per line (v5)
+    constexpr std::size_t smem = K3Smem<N, EPI>::bytes;
+    static bool configured = false;
+    if (!configured) {
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_v5<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = true;
+    }
+    k_sem_k1_v5<N, EPI><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
+  } else if constexpr (MODE == SEM_AX && N >= 5) {
     // persistent register-blocked line kernel, double-buffered TMA / cp.async prefetch
     constexpr std::size_t smem = K4Smem<N, EPI>::bytes;
     constexpr int nt = (N + 1) * (N + 1);
