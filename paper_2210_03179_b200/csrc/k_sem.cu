@@ -825,6 +825,8 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_v5(SemArgs A) 
 #undef CD
 }
 
+#include "k_sem_k1.cuh"
+
 // ---------------------------------------------------------------- K1 (LVEC mode: assemble an L-vector)
 template <int N, int EPI>
 __global__ void k_sem_k1_lvec(SemArgs A) {
@@ -847,9 +849,41 @@ __global__ void k_sem_k1_lvec(SemArgs A) {
 }
 
 // ---------------------------------------------------------------- K2
+// Contributor table per shared slot s: up to 8 packed entries
+// (shell index | dx<<16 | dy<<17 | dz<<18) in the fixed (dz, dy, dx) order,
+// so every contribution load is independent (no lut -> shell dependency).
+template <int N>
+struct K2Table {
+  static constexpr int NSH = sem_nshared(N);
+  int cnt[NSH];
+  int ent[NSH][8];
+};
+
+template <int N>
+__device__ __forceinline__ void k2_build_table(K2Table<N>* T, const int* lut) {
+  constexpr int N1 = N + 1, NSH = sem_nshared(N);
+  for (int s = threadIdx.x; s < NSH; s += blockDim.x) {
+    int a, b, c;
+    sem_shared_abc(N, s, a, b, c);
+    const int i = a + 1, j = b + 1, k = c + 1;
+    const int nz = (k == N) ? 2 : 1, ny = (j == N) ? 2 : 1, nx = (i == N) ? 2 : 1;
+    int n = 0;
+    for (int dz = 0; dz < nz; ++dz)
+      for (int dy = 0; dy < ny; ++dy)
+        for (int dx = 0; dx < nx; ++dx) {
+          const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
+          T->ent[s][n++] = lut[(lk * N1 + lj) * N1 + li] | (dx << 16) | (dy << 17) | (dz << 18);
+        }
+    T->cnt[s] = n;
+  }
+}
+
 template <int N, int EPI>
 __global__ void k_sem_k2(SemArgs A) {
   constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N), NSH = sem_nshared(N);
+  __shared__ K2Table<N> T;
+  k2_build_table<N>(&T, A.lut);
+  __syncthreads();
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long q = tid / NSH;
   const int s = (int)(tid - q * NSH);
@@ -860,22 +894,26 @@ __global__ void k_sem_k2(SemArgs A) {
   sem_shared_abc(N, s, a, b, c);
   // padding (far domain boundary) is not an unknown
   if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
-  const int i = a + 1, j = b + 1, k = c + 1;
-  const int nz = (k == N) ? 2 : 1, ny = (j == N) ? 2 : 1, nx = (i == N) ? 2 : 1;
-  double sum = 0.0;
-  for (int dz = 0; dz < nz; ++dz)
-    for (int dy = 0; dy < ny; ++dy)
-      for (int dx = 0; dx < nx; ++dx) {
-        const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
-        double v;
-        if (ez + dz >= A.Ezl) {
-          v = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + li + N1 * lj];
-        } else {
-          const long e2 = e + dx + (long)A.Ex * (dy + (long)A.Ey * dz);
-          v = A.shell[e2 * A.nshell + A.lut[(lk * N1 + lj) * N1 + li]];
-        }
-        sum += v;
+  const int n = T.cnt[s];
+  double vals[8];
+#pragma unroll
+  for (int cidx = 0; cidx < 8; ++cidx) {
+    if (cidx < n) {
+      const int p = T.ent[s][cidx];
+      const int li = p & 0xffff, dx = (p >> 16) & 1, dy = (p >> 17) & 1, dz = (p >> 18) & 1;
+      if (ez + dz >= A.Ezl) {
+        // halo: k=0 face of the layer above, indexed by (ex', ey', i', j')
+        const int i2 = (a + 1) - dx * N, j2 = (b + 1) - dy * N;
+        vals[cidx] = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + i2 + N1 * j2];
+      } else {
+        vals[cidx] = A.shell[(e + dx + (long)A.Ex * (dy + (long)A.Ey * dz)) * A.nshell + li];
       }
+    }
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int cidx = 0; cidx < 8; ++cidx)
+    if (cidx < n) sum += vals[cidx];
   const long slot = e * NOS + NINT + s;
   double dv = 0.0, o0 = 0.0, o1 = 0.0, o2 = 0.0;
   if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) {
@@ -900,10 +938,10 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
     constexpr std::size_t smem = K3Smem<N, EPI>::bytes;
     static bool configured = false;
     if (!configured) {
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_v5<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       configured = true;
     }
-    k_sem_k1_v5<N, EPI><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
+    k_sem_k1_lines<N, EPI><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
   } else if constexpr (MODE == SEM_AX && N >= 5) {
     // persistent register-blocked line kernel, double-buffered TMA / cp.async prefetch
     constexpr std::size_t smem = K4Smem<N, EPI>::bytes;
