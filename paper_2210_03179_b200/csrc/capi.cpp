@@ -193,6 +193,97 @@ void chebyshev_smooth(cmg_op* A, const double* invd, const cmg_cheb_config& cfg,
   if (d != A->s_d.p) std::swap(A->s_d.p, A->s_d2.p);
 }
 
+// smoothers.hpp:95-148 with the diagonal S replaced by an operator (Schwarz):
+// same recurrences and coefficients as chebyshev_smooth, unfused.
+void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& cfg, std::size_t order,
+                        const double* b, double* x, bool x_is_zero) {
+  if (order == 0) return;
+  validate_cheb(cfg);
+  A->ensure_scratch();
+  cmg_ctx* c = A->ctx;
+  cudaStream_t s = c->stream;
+  const std::size_t L = A->len;
+  double* r = A->s_r.p;
+  double* d = A->s_d.p;
+  double* t = A->s_t.p;
+  double* sv = c->workspace(7, L);
+  const double lmax = cfg.lambda_max_multiplier * cfg.lambda_tilde;
+  if (x_is_zero) CMG_CUDA(cudaMemcpyAsync(r, b, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  else A->residual(b, x, r);
+  bool xz = x_is_zero;
+  if (is_fourth(cfg.family)) {  // smoothers.hpp:126-148
+    const double* beta = nullptr;
+    if (cfg.family == CMG_FOURTH_OPT) {
+      beta = host_beta_row(order);
+      if (!beta)
+        fail(CMG_ERANGE, "beta_coefficients: order " + std::to_string(order) + " outside tabulated range 1..20");
+    }
+    const double inv_lmax = 1.0 / lmax;
+    S(sctx, r, sv);
+    launch_scal_copy(L, nullptr, (4.0 / 3.0) * inv_lmax, sv, d, s);
+    for (std::size_t it = 1; it < order; ++it) {
+      const double bi = beta ? beta[it - 1] : 1.0;
+      if (xz) launch_scal_copy(L, nullptr, bi, d, x, s);
+      else launch_axpy(L, bi, d, x, s);
+      xz = false;
+      A->apply(d, t);
+      launch_axpy(L, -1.0, t, r, s);
+      const double fi = static_cast<double>(it);
+      const double c1 = (2.0 * fi - 1.0) / (2.0 * fi + 3.0);
+      const double c2 = (8.0 * fi + 4.0) / (2.0 * fi + 3.0) * inv_lmax;
+      S(sctx, r, sv);
+      launch_lincomb(L, c1, d, c2, sv, d, s);
+    }
+    vec_final_update(L, beta ? beta[order - 1] : 1.0, xz, d, x, s);
+  } else {  // smoothers.hpp:95-120
+    const double lmin = cfg.lambda_min_multiplier * cfg.lambda_tilde;
+    const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma = theta / delta;
+    double rho_prev = 1.0 / sigma;
+    S(sctx, r, sv);  // z = S r (r holds the residual); keep z in r
+    CMG_CUDA(cudaMemcpyAsync(r, sv, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    launch_scal_copy(L, nullptr, 1.0 / theta, r, d, s);
+    for (std::size_t it = 1; it < order; ++it) {
+      if (xz) CMG_CUDA(cudaMemcpyAsync(x, d, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      else launch_axpy(L, 1.0, d, x, s);
+      xz = false;
+      A->apply(d, t);
+      S(sctx, t, sv);
+      launch_axpy(L, -1.0, sv, r, s);
+      const double rho = 1.0 / (2.0 * sigma - rho_prev);
+      launch_lincomb(L, rho * rho_prev, d, 2.0 * rho / delta, r, d, s);
+      rho_prev = rho;
+    }
+    vec_final_update(L, 1.0, xz, d, x, s);
+  }
+}
+
+// smoothers.hpp:61-79 with S an operator
+double estimate_lambda_max_S(cmg_op* A, SApply S, void* sctx, std::size_t iterations, std::uint64_t seed) {
+  if (iterations < 1) fail(CMG_EINVAL, "estimate_lambda_max: iterations must be >= 1");
+  cmg_ctx* c = A->ctx;
+  std::vector<double> v0(A->n);
+  host_random_vector(A->n, seed, v0.data());
+  DBuf v(A->len), w(A->len), t(A->len);
+  v.zero(c->stream);
+  w.zero(c->stream);
+  t.zero(c->stream);
+  A->upload_canonical(v0.data(), v.p);
+  double* nrm = c->dscal + S_TMP0;
+  for (std::size_t it = 0; it < iterations; ++it) {
+    A->apply(v.p, t.p);
+    S(sctx, t.p, w.p);
+    A->norm2(w.p, nrm);
+    launch_div_scalar_dev(A->len, w.p, nrm, v.p, c->stream);
+  }
+  A->apply(v.p, t.p);
+  S(sctx, t.p, w.p);
+  A->dot(v.p, w.p, c->dscal + S_TMP0);
+  A->dot(v.p, v.p, c->dscal + S_TMP1);
+  CMG_CUDA(cudaMemcpyAsync(c->hpin, c->dscal + S_TMP0, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  return c->hpin[0] / c->hpin[1];
+}
+
 // smoothers.hpp:61-79
 double estimate_lambda_max(cmg_op* A, const double* invd, std::size_t iterations,
                            std::uint64_t seed) {
@@ -348,7 +439,8 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
   const int m = static_cast<int>(o.restart);
   Report R;
   R.mv0 = A->count;
-  DBuf xb(L), r(L), V((m + 1) * L), Z(m * L), w(L), rt(L), xj(L);
+  WBuf xb = wsbuf(c, 0, L), r = wsbuf(c, 1, L), V = wsbuf(c, 2, (m + 1) * L), Z = wsbuf(c, 3, m * L),
+       w = wsbuf(c, 4, L), rt = wsbuf(c, 5, L), xj = wsbuf(c, 6, L);
   xb.zero(s); r.zero(s); w.zero(s); rt.zero(s); xj.zero(s);
   bool x0zero = true;
   if (x0) {
@@ -436,7 +528,8 @@ void pcg(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double* x
   const std::size_t L = A->len;
   Report R;
   R.mv0 = A->count;
-  DBuf xb(L), r(L), z(L), p(L), Ap(L), rt(L);
+  WBuf xb = wsbuf(c, 0, L), r = wsbuf(c, 1, L), z = wsbuf(c, 2, L), p = wsbuf(c, 3, L),
+       Ap = wsbuf(c, 4, L), rt = wsbuf(c, 5, L);
   xb.zero(s); r.zero(s); z.zero(s); p.zero(s); Ap.zero(s); rt.zero(s);
   double* dsc = c->dscal;
   int* stop = c->dflag;
@@ -533,7 +626,7 @@ void stationary(cmg_op* A, cmg_precond* M, const double* b, double tol, std::siz
   const std::size_t L = A->len;
   Report R;
   R.mv0 = A->count;
-  DBuf x(L), r(L), z(L);
+  WBuf x = wsbuf(c, 0, L), r = wsbuf(c, 1, L), z = wsbuf(c, 2, L);
   x.zero(s); z.zero(s);
   CMG_CUDA(cudaMemcpyAsync(r.p, b, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
   double* dsc = c->dscal;

@@ -80,6 +80,9 @@ void launch_div_scalar_dev(std::size_t n, const double* x, const double* s_dev, 
                            cudaStream_t s);  // y = x / *s
 void launch_any_zero(std::size_t n, const double* d, int* flag, cudaStream_t s);
 void launch_any_nonzero(std::size_t n, const double* d, int* flag, cudaStream_t s);
+// out = c1 d + c2 s   (Chebyshev direction update with a general smoother)
+void launch_lincomb(std::size_t n, double c1, const double* d, double c2, const double* s, double* out,
+                    cudaStream_t st);
 
 // ---------------------------------------------------------------- Krylov helpers
 // CGS: w -= sum_l coef[l] V_l ; h[l*hstride] += coef[l]

@@ -75,8 +75,29 @@ struct cmg_ctx {
   double* hpin = nullptr;    // pinned readback area: 64 doubles
   std::unique_ptr<cmg::Comm> comm;
   int rank = 0, nranks = 1;
+  // Krylov workspace cache: grown on demand, reused across solves (a PGMRES(30)
+  // basis at E=64^3 is 44 GB -- allocating it per solve would dominate).
+  std::vector<std::unique_ptr<cmg::DBuf>> ws;
+  double* workspace(int slot, std::size_t n) {
+    if (static_cast<int>(ws.size()) <= slot) ws.resize(slot + 1);
+    if (!ws[slot]) ws[slot] = std::make_unique<cmg::DBuf>();
+    if (ws[slot]->n < n) ws[slot]->alloc(n);
+    return ws[slot]->p;
+  }
   void sync() { CMG_CUDA(cudaStreamSynchronize(stream)); }
 };
+
+namespace cmg {
+// view of a workspace slot with the DBuf interface used by the drivers
+struct WBuf {
+  double* p;
+  std::size_t n;
+  void zero(cudaStream_t s) {
+    if (n) CMG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(double), s));
+  }
+};
+inline WBuf wsbuf(cmg_ctx* c, int slot, std::size_t n) { return WBuf{c->workspace(slot, n), n}; }
+}  // namespace cmg
 
 // LinearOperatorLike on device vectors (operators.hpp:19-26).  `n` is the
 // number of unknowns (rows()), `len` the storage length of a device vector.
@@ -165,4 +186,16 @@ void host_deriv_matrix(int N, const double* xi, double* D);
 void host_interp_matrix(int Nf, int Nc, double* J);
 // generalized symmetric eigenproblem A s = lam B s with B SPD (dense, n small)
 void host_sym_geneig(int n, const double* A, const double* B, double* S, double* lam);
+void host_node_coords(int geometry, double eps, const double* xi, int Ex, int Ey, int Ez, int ex, int ey,
+                      int ez, int i, int j, int k, double* X, double* Y, double* Z);
+void host_element_lengths(int geometry, double eps, int N, const double* xi, int Ex, int Ey, int Ez, int ex,
+                          int ey, int ez, double* L);
+void host_fdm_1d(int N, const double* w, const double* D, double Ll, double L, double Lr, int dl, int d0,
+                 int dN, int dr, double* S, double* lam);
+// Chebyshev smoothing / power iteration with a general smoother operator S
+// (S(in, out): out = S in) -- the Schwarz path
+using SApply = void (*)(void* ctx, const double* in, double* out);
+void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& cfg, std::size_t order,
+                        const double* b, double* x, bool x_is_zero);
+double estimate_lambda_max_S(cmg_op* A, SApply S, void* sctx, std::size_t iterations, std::uint64_t seed);
 }  // namespace cmg

@@ -235,6 +235,99 @@ void host_interp_matrix(int Nf, int Nc, double* J) {
     }
 }
 
+// ---- geometry on the host (Schwarz box approximation only; the device computes the factors) ----
+static double kr_right(double eps, double x) { return (x <= 0.5) ? (2.0 - eps) * x : 1.0 + eps * (x - 1.0); }
+static double kr_left(double eps, double x) { return 1.0 - kr_right(eps, 1.0 - x); }
+static double kr_step(double a, double b, double x) {
+  if (x <= 0.0) return a;
+  if (x >= 1.0) return b;
+  return a + (b - a) * (x * x * x * (x * (6.0 * x - 15.0) + 10.0));
+}
+
+void host_node_coords(int geometry, double eps, const double* xi, int Ex, int Ey, int Ez, int ex, int ey,
+                      int ez, int i, int j, int k, double* X, double* Y, double* Z) {
+  const double x = (ex + 0.5 * (xi[i] + 1.0)) / Ex, y = (ey + 0.5 * (xi[j] + 1.0)) / Ey,
+               z = (ez + 0.5 * (xi[k] + 1.0)) / Ez;
+  double u = x, v = y, w = z;
+  if (geometry == 1) {  // Kershaw map, as k_sem.cu / oracle_sem.c
+    int layer = static_cast<int>(x * 6.0);
+    if (layer > 5) layer = 5;
+    const double lam = (x - layer / 6.0) * 6.0;
+    switch (layer) {
+      case 0: v = kr_left(eps, y); w = kr_left(eps, z); break;
+      case 1:
+      case 4:
+        v = kr_step(kr_left(eps, y), kr_right(eps, y), lam);
+        w = kr_step(kr_left(eps, z), kr_right(eps, z), lam);
+        break;
+      case 2:
+        v = kr_step(kr_right(eps, y), kr_left(eps, y), lam / 2.0);
+        w = kr_step(kr_right(eps, z), kr_left(eps, z), lam / 2.0);
+        break;
+      case 3:
+        v = kr_step(kr_right(eps, y), kr_left(eps, y), (1.0 + lam) / 2.0);
+        w = kr_step(kr_right(eps, z), kr_left(eps, z), (1.0 + lam) / 2.0);
+        break;
+      default: v = kr_right(eps, y); w = kr_right(eps, z); break;
+    }
+  }
+  *X = u - 0.5;
+  *Y = v - 0.5;
+  *Z = w - 0.5;
+}
+
+// box approximation of an element: mean length of its 4 edges per direction
+void host_element_lengths(int geometry, double eps, int N, const double* xi, int Ex, int Ey, int Ez, int ex,
+                          int ey, int ez, double* L) {
+  double P[8][3];
+  for (int v = 0; v < 8; ++v)
+    host_node_coords(geometry, eps, xi, Ex, Ey, Ez, ex, ey, ez, (v & 1) ? N : 0, (v & 2) ? N : 0,
+                     (v & 4) ? N : 0, &P[v][0], &P[v][1], &P[v][2]);
+  for (int d = 0; d < 3; ++d) {
+    const int bit = 1 << d;
+    double s = 0.0;
+    for (int v = 0; v < 8; ++v)
+      if (!(v & bit)) {
+        const double dx = P[v | bit][0] - P[v][0], dy = P[v | bit][1] - P[v][1], dz = P[v | bit][2] - P[v][2];
+        s += std::sqrt(dx * dx + dy * dy + dz * dz);
+      }
+    L[d] = 0.25 * s;
+  }
+}
+
+// 1D extended-element operators of the Schwarz subdomain (PAPER.md:579-617,
+// definition in oracle/oracle_schwarz.c): 3-element patch stiffness / GLL mass
+// restricted to the N+3 extended nodes, Dirichlet-eliminated nodes decoupled.
+void host_fdm_1d(int N, const double* w, const double* D, double Ll, double L, double Lr, int dl, int d0,
+                 int dN, int dr, double* S, double* lam) {
+  const int n1 = N + 1, pb = N + 3, np = 3 * N + 1;
+  std::vector<double> K(np * np, 0.0), M(np, 0.0);
+  const double Ls[3] = {Ll, L, Lr};
+  for (int el = 0; el < 3; ++el) {
+    const double h = Ls[el];
+    for (int a = 0; a < n1; ++a) {
+      M[el * N + a] += 0.5 * h * w[a];
+      for (int b = 0; b < n1; ++b) {
+        double kab = 0.0;
+        for (int m = 0; m < n1; ++m) kab += D[m * n1 + a] * w[m] * D[m * n1 + b];
+        K[(el * N + a) * np + (el * N + b)] += (2.0 / h) * kab;
+      }
+    }
+  }
+  std::vector<double> A(pb * pb), B(pb * pb, 0.0);
+  std::vector<int> dir(pb, 0);
+  if (dl) dir[0] = 1;
+  if (d0) dir[0] = dir[1] = 1;
+  if (dN) dir[pb - 1] = dir[pb - 2] = 1;
+  if (dr) dir[pb - 1] = 1;
+  for (int a = 0; a < pb; ++a) {
+    B[a * pb + a] = dir[a] ? 1.0 : M[N - 1 + a];
+    for (int b = 0; b < pb; ++b)
+      A[a * pb + b] = (dir[a] || dir[b]) ? (a == b ? 1.0 : 0.0) : K[(N - 1 + a) * np + (N - 1 + b)];
+  }
+  host_sym_geneig(pb, A.data(), B.data(), S, lam);
+}
+
 // cyclic Jacobi on a symmetric matrix (destroyed); eigenvectors in columns of V
 static void sym_eig(int n, double* A, double* lam, double* V) {
   for (int i = 0; i < n; ++i)

@@ -348,6 +348,20 @@ void launch_any_zero(std::size_t n, const double* d, int* flag, cudaStream_t s) 
   CMG_LAUNCH_CHECK();
 }
 namespace {
+__global__ void k_lincomb(std::size_t n, double c1, const double* __restrict__ d, double c2,
+                          const double* __restrict__ s, double* __restrict__ out) {
+  for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
+       i += (std::size_t)gridDim.x * blockDim.x)
+    out[i] = c1 * d[i] + c2 * s[i];
+}
+}  // namespace
+void launch_lincomb(std::size_t n, double c1, const double* d, double c2, const double* s, double* out,
+                    cudaStream_t st) {
+  k_lincomb<<<vgrid(n), 256, 0, st>>>(n, c1, d, c2, s, out);
+  CMG_LAUNCH_CHECK();
+}
+
+namespace {
 __global__ void k_any_nonzero(std::size_t n, const double* __restrict__ d, int* flag) {
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
        i += (std::size_t)gridDim.x * blockDim.x)

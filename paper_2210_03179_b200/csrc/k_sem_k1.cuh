@@ -5,40 +5,32 @@
 // One element per block of 2(N+1)^2 threads.  Every tensor contraction is a
 // "line contraction": the N+1 values of a line along the contracted direction
 // are loaded once from shared memory and multiplied by the GLL derivative
-// matrix held in __constant__ memory (DFMA uniform-register operands, no
-// shared traffic for D).  Each line is split between two threads (half H of
-// the outputs each), H is a template parameter so every D index is a
-// compile-time constant.
+// matrix held in __constant__ memory (no shared traffic for D).  Each line is
+// split between two threads (half H of the outputs each); the phases between
+// barriers are templates on H so every D index is a compile-time constant,
+// and the barriers themselves stay in uniform control flow.
 //   1. thread 0: TMA bulk copies of the element's 6 geometric factors
 //      (24.6 KB at N=7) and of the interior blocks of the epilogue operands;
 //   2. all threads: branch-free gather of Q u (all loads issued before any
 //      store, so the element pays one memory latency, not KH);
-//   3. gradient (r rows, s columns, t in registers) -> G_e grad u;
-//   4. divergence (r rows, s columns accumulate, t in registers) ->
+//   3. gradient (r rows, s columns, t on the thread's column) -> G_e grad u;
+//   4. divergence (r rows, s columns accumulate, t on the column) ->
 //      epilogue: interior nodes finished in place, shell nodes to K2.
 
-template <int N, int EPI, int H>
-__device__ __forceinline__ void k1_body(const SemArgs& A, double* sm, int line, long e) {
+template <int N, int EPI>
+struct K1L {
   using S = K3Smem<N, EPI>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
-  constexpr int R = N1 + 1;
-  constexpr int KH = N1 / 2, O0 = H * KH;
-#define IDX(i, j, k) (((k) * N1 + (j)) * R + (i))
-#define CD(a, b) c_D[N][(a) * N1 + (b)]
-  double* sG = sm + S::g_off;
-  double* so = sm + S::o_off;
-  double* su = sm + S::u_off;
-  double* sr = sm + S::r_off;
-  double* ss = sm + S::s_off;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
-  const int ta = line % N1, tb = line / N1;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-  // 2. gather: thread (i,j,H) owns k in [O0, O0+KH)
-  {
-    const int i = ta, j = tb;
+  static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
+  static constexpr int R = N1 + 1, KH = N1 / 2;
+  __device__ static constexpr int idx(int i, int j, int k) { return ((k * N1 + j) * R + i); }
+
+  template <int H>
+  __device__ static void gather(const SemArgs& A, double* su, int ta, int tb, long e) {
+    constexpr int O0 = H * KH;
+    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
     int oex = 0, oey = 0;
-    const int ax = owner1d<N>(ex, i, A.Ex, oex);
-    const int ay = owner1d<N>(ey, j, A.Ey, oey);
+    const int ax = owner1d<N>(ex, ta, A.Ex, oex);
+    const int ay = owner1d<N>(ey, tb, A.Ey, oey);
     const bool xy_ok = ax >= 0 && ay >= 0;
     const double* ptr[KH];
     bool ok[KH];
@@ -57,126 +49,139 @@ __device__ __forceinline__ void k1_body(const SemArgs& A, double* sm, int line, 
 #pragma unroll
     for (int q = 0; q < KH; ++q) v[q] = ok[q] ? __ldg(ptr[q]) : 0.0;
 #pragma unroll
-    for (int q = 0; q < KH; ++q) su[IDX(i, j, O0 + q)] = v[q];
+    for (int q = 0; q < KH; ++q) su[idx(ta, tb, O0 + q)] = v[q];
   }
-  __syncthreads();
-  // 3. gradient
-  double wt[KH], dvh[KH];
-  {
+
+  template <int H>
+  __device__ static void gradient(const double* su, double* sr, double* ss, int ta, int tb, double* wt,
+                                  double* dvh) {
+    constexpr int O0 = H * KH;
     double l[N1];
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(m, ta, tb)];
+    for (int m = 0; m < N1; ++m) l[m] = su[idx(m, ta, tb)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(O0 + q, m) * l[m];
-      sr[IDX(O0 + q, ta, tb)] = v;
+      for (int m = 0; m < N1; ++m) v += c_D[N][(O0 + q) * N1 + m] * l[m];
+      sr[idx(O0 + q, ta, tb)] = v;
     }
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, m, tb)];
+    for (int m = 0; m < N1; ++m) l[m] = su[idx(ta, m, tb)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(O0 + q, m) * l[m];
-      ss[IDX(ta, O0 + q, tb)] = v;
+      for (int m = 0; m < N1; ++m) v += c_D[N][(O0 + q) * N1 + m] * l[m];
+      ss[idx(ta, O0 + q, tb)] = v;
     }
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, tb, m)];
+    for (int m = 0; m < N1; ++m) l[m] = su[idx(ta, tb, m)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(O0 + q, m) * l[m];
+      for (int m = 0; m < N1; ++m) v += c_D[N][(O0 + q) * N1 + m] * l[m];
       wt[q] = v;
       dvh[q] = l[O0 + q];
     }
   }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  {
-    const int i = ta, j = tb;
+
+  template <int H>
+  __device__ static void geometry(const double* sG, double* sr, double* ss, int i, int j, double* wt) {
+    constexpr int O0 = H * KH;
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       const int k = O0 + q;
       const int l = (k * N1 + j) * N1 + i;
-      const double ur = sr[IDX(i, j, k)], us = ss[IDX(i, j, k)], ut = wt[q];
+      const double ur = sr[idx(i, j, k)], us = ss[idx(i, j, k)], ut = wt[q];
       const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
       const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
-      sr[IDX(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
-      ss[IDX(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
+      sr[idx(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
+      ss[idx(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
       wt[q] = g2 * ur + g4 * us + g5 * ut;
     }
   }
-  __syncthreads();
-  // 4. divergence
-  {
+
+  template <int H>
+  __device__ static void div_r(const double* sr, double* su, int ta, int tb) {
+    constexpr int O0 = H * KH;
     double l[N1];
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = sr[IDX(m, ta, tb)];
+    for (int m = 0; m < N1; ++m) l[m] = sr[idx(m, ta, tb)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, O0 + q) * l[m];
-      su[IDX(O0 + q, ta, tb)] = v;
+      for (int m = 0; m < N1; ++m) v += c_D[N][m * N1 + (O0 + q)] * l[m];
+      su[idx(O0 + q, ta, tb)] = v;
     }
   }
-  __syncthreads();
+
+  template <int H>
+  __device__ static void div_s(const double* ss, double* su, double* sr, int ta, int tb, const double* wt) {
+    constexpr int O0 = H * KH;
 #pragma unroll
-  for (int q = 0; q < KH; ++q) sr[IDX(ta, tb, O0 + q)] = wt[q];
-  {
+    for (int q = 0; q < KH; ++q) sr[idx(ta, tb, O0 + q)] = wt[q];  // publish w_t columns
     double l[N1];
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = ss[IDX(ta, m, tb)];
+    for (int m = 0; m < N1; ++m) l[m] = ss[idx(ta, m, tb)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, O0 + q) * l[m];
-      su[IDX(ta, O0 + q, tb)] += v;
+      for (int m = 0; m < N1; ++m) v += c_D[N][m * N1 + (O0 + q)] * l[m];
+      su[idx(ta, O0 + q, tb)] += v;
     }
   }
-  __syncthreads();
-  const int i = ta, j = tb;
-  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
-  double l[N1];
+
+  template <int H>
+  __device__ static void finish(const SemArgs& A, const double* su, const double* sr, const double* so, int i,
+                                int j, long e, const double* dvh) {
+    constexpr int O0 = H * KH;
+    const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+    double l[N1];
 #pragma unroll
-  for (int m = 0; m < N1; ++m) l[m] = sr[IDX(i, j, m)];
+    for (int m = 0; m < N1; ++m) l[m] = sr[idx(i, j, m)];
 #pragma unroll
-  for (int q = 0; q < KH; ++q) {
-    const int k = O0 + q;
-    double v = 0.0;
+    for (int q = 0; q < KH; ++q) {
+      const int k = O0 + q;
+      double v = 0.0;
 #pragma unroll
-    for (int m = 0; m < N1; ++m) v += CD(m, O0 + q) * l[m];
-    v += su[IDX(i, j, k)];
-    if (ij_interior && k >= 1 && k < N) {
-      const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      if constexpr (NOPS > 0) a0 = so[p];
-      if constexpr (NOPS > 1) a1 = so[NIP + p];
-      if constexpr (NOPS > 2) a2 = so[2 * NIP + p];
-      epilogue<EPI>(A, e * NOS + p, v, dvh[q], a0, a1, a2);
-    } else {
-      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
+      for (int m = 0; m < N1; ++m) v += c_D[N][m * N1 + k] * l[m];
+      v += su[idx(i, j, k)];
+      if (ij_interior && k >= 1 && k < N) {
+        const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if constexpr (NOPS > 0) a0 = so[p];
+        if constexpr (NOPS > 1) a1 = so[NIP + p];
+        if constexpr (NOPS > 2) a2 = so[2 * NIP + p];
+        epilogue<EPI>(A, e * NOS + p, v, dvh[q], a0, a1, a2);
+      } else {
+        A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
+      }
     }
   }
-#undef IDX
-#undef CD
-}
+};
 
 template <int N, int EPI>
 __global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_lines(SemArgs A) {
-  using S = K3Smem<N, EPI>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
+  using L = K1L<N, EPI>;
+  using S = typename L::S;
+  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP, KH = L::KH;
   extern __shared__ __align__(128) double sm[];
+  double* sG = sm + S::g_off;
+  double* so = sm + S::o_off;
+  double* su = sm + S::u_off;
+  double* sr = sm + S::r_off;
+  double* ss = sm + S::s_off;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
   const int t = threadIdx.x;
   const long e = A.e_begin + blockIdx.x;
+  const int line = t % (N1 * N1);
+  const bool h0 = t < N1 * N1;  // warp-uniform half selector
+  const int ta = line % N1, tb = line / N1;
   if (t == 0) {  // 1. TMA
-    double* sG = sm + S::g_off;
-    double* so = sm + S::o_off;
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
     const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
     unsigned bytes = 6 * NP * sizeof(double);
     if constexpr (NOPS > 0 && sem_nint(N) > 0) bytes += (NOPS - (skip_x ? 1 : 0)) * NIP * 8;
@@ -191,7 +196,23 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_lines(SemArgs 
       }
     }
   }
-  const int line = t % (N1 * N1);
-  if (t < N1 * N1) k1_body<N, EPI, 0>(A, sm, line, e);  // warp-uniform split
-  else k1_body<N, EPI, 1>(A, sm, line, e);
+  if (h0) L::template gather<0>(A, su, ta, tb, e);
+  else L::template gather<1>(A, su, ta, tb, e);
+  __syncthreads();
+  double wt[KH], dvh[KH];
+  if (h0) L::template gradient<0>(su, sr, ss, ta, tb, wt, dvh);
+  else L::template gradient<1>(su, sr, ss, ta, tb, wt, dvh);
+  __syncthreads();
+  mbar_wait(bar, 0);
+  if (h0) L::template geometry<0>(sG, sr, ss, ta, tb, wt);
+  else L::template geometry<1>(sG, sr, ss, ta, tb, wt);
+  __syncthreads();
+  if (h0) L::template div_r<0>(sr, su, ta, tb);
+  else L::template div_r<1>(sr, su, ta, tb);
+  __syncthreads();
+  if (h0) L::template div_s<0>(ss, su, sr, ta, tb, wt);
+  else L::template div_s<1>(ss, su, sr, ta, tb, wt);
+  __syncthreads();
+  if (h0) L::template finish<0>(A, su, sr, so, ta, tb, e, dvh);
+  else L::template finish<1>(A, su, sr, so, ta, tb, e, dvh);
 }

@@ -12,7 +12,9 @@
 // V-cycle control flow (multigrid.hpp:69-90) applied recursively.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -384,6 +386,14 @@ struct cmg_pmg {
   // coarse FDM (p=1 box): S_d, lam_d per dimension, D grid over the full p=1 slot array
   DBuf Sx, Sy, Sz, Dg, cfull, t1, t2;
   DBuf cg_r, cg_z, cg_p, cg_Ap;  // deformed-mesh coarse CG
+  // Schwarz smoother data per smoothed level
+  struct Schwarz {
+    DBuf S, lam, Lout, wmult;
+    IBuf sidx;
+    cmg_pmg* p = nullptr;
+    int level = 0;
+  };
+  std::vector<std::unique_ptr<Schwarz>> sch;
   int cnx = 0, cny = 0, cnz = 0;
 };
 
@@ -498,9 +508,109 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
   c->count = cnt0;  // coarse-level applications are not fine matvecs
 }
 
+// ---- Schwarz (ASM / RAS) smoother, PAPER.md:560-629 ----
+void schwarz_setup(cmg_pmg* p, int l) {
+  SemLevel* L = p->lev[l].get();
+  if (L->distributed()) fail(CMG_EINVAL, "pmg: Schwarz smoothers run on one GPU (BASELINE configs[2])");
+  auto sc = std::make_unique<cmg_pmg::Schwarz>();
+  sc->p = p;
+  sc->level = l;
+  const int N = L->N, N1 = N + 1, pb = N + 3;
+  std::vector<double> xi(N1), w(N1), D(N1 * N1);
+  host_gll(N, xi.data(), w.data());
+  host_deriv_matrix(N, xi.data(), D.data());
+  const int ne[3] = {L->Ex, L->Ey, L->Ez};
+  // element box lengths
+  std::vector<double> Lel(static_cast<std::size_t>(L->E) * 3);
+  for (long e = 0; e < L->E; ++e) {
+    const int ex = static_cast<int>(e % L->Ex), ey = static_cast<int>((e / L->Ex) % L->Ey),
+              ez = static_cast<int>(e / (static_cast<long>(L->Ex) * L->Ey));
+    host_element_lengths(L->desc.geometry, L->desc.eps, N, xi.data(), L->Ex, L->Ey, L->Ez, ex, ey, ez,
+                         &Lel[e * 3]);
+  }
+  // 1D FDM bases, deduplicated on (Ll, L, Lr, boundary flags)
+  std::map<std::tuple<double, double, double, int>, int> uniq;
+  std::vector<double> Sall, lall;
+  std::vector<int> sidx(static_cast<std::size_t>(L->E) * 3);
+  std::vector<double> Sd(pb * pb), ld(pb);
+  for (long e = 0; e < L->E; ++e) {
+    const int ec[3] = {static_cast<int>(e % L->Ex), static_cast<int>((e / L->Ex) % L->Ey),
+                       static_cast<int>(e / (static_cast<long>(L->Ex) * L->Ey))};
+    for (int d = 0; d < 3; ++d) {
+      const long stride = d == 0 ? 1 : (d == 1 ? L->Ex : static_cast<long>(L->Ex) * L->Ey);
+      const double Lc = Lel[e * 3 + d];
+      const double Ll = ec[d] > 0 ? Lel[(e - stride) * 3 + d] : Lc;
+      const double Lr = ec[d] + 1 < ne[d] ? Lel[(e + stride) * 3 + d] : Lc;
+      const int g0 = ec[d] * N, gmax = N * ne[d];
+      const int dl = (g0 - 1) <= 0, d0 = g0 == 0, dN = g0 + N == gmax, dr = (g0 + N + 1) >= gmax;
+      const int flags = dl | (d0 << 1) | (dN << 2) | (dr << 3);
+      const auto key = std::make_tuple(Ll, Lc, Lr, flags);
+      auto it = uniq.find(key);
+      if (it == uniq.end()) {
+        host_fdm_1d(N, w.data(), D.data(), Ll, Lc, Lr, dl, d0, dN, dr, Sd.data(), ld.data());
+        it = uniq.emplace(key, static_cast<int>(uniq.size())).first;
+        Sall.insert(Sall.end(), Sd.begin(), Sd.end());
+        lall.insert(lall.end(), ld.begin(), ld.end());
+      }
+      sidx[e * 3 + d] = it->second;
+    }
+  }
+  sc->S.alloc(Sall.size());
+  sc->lam.alloc(lall.size());
+  CMG_CUDA(cudaMemcpy(sc->S.p, Sall.data(), Sall.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CMG_CUDA(cudaMemcpy(sc->lam.p, lall.data(), lall.size() * sizeof(double), cudaMemcpyHostToDevice));
+  sc->sidx.upload(sidx);
+  const bool ras = p->smoother == 2;
+  sc->Lout.alloc(static_cast<std::size_t>(L->E) * (ras ? N1 * N1 * N1 : pb * pb * pb));
+  if (ras) {  // W = 1 / element multiplicity (assembled count of local copies)
+    DBuf ones(static_cast<std::size_t>(L->E) * N1 * N1 * N1), cnt(L->len);
+    launch_set(ones.n, 1.0, ones.p, p->ctx->stream);
+    cnt.zero(p->ctx->stream);
+    SemArgs a = L->args();
+    a.lvec = ones.p;
+    a.y = cnt.p;
+    L->run(SEM_LVEC, EPI_STORE, a);
+    sc->wmult.alloc(L->len);
+    sem_inverse_diag(L->args(), cnt.p, sc->wmult.p, p->ctx->dflag + 13, p->ctx->stream);
+    p->ctx->sync();
+  }
+  if (static_cast<int>(p->sch.size()) <= l) p->sch.resize(l + 1);
+  p->sch[l] = std::move(sc);
+}
+
+// out = S_ASM r or S_RAS r on level l
+void schwarz_apply(void* vctx, const double* r, double* out) {
+  auto* sc = static_cast<cmg_pmg::Schwarz*>(vctx);
+  cmg_pmg* p = sc->p;
+  SemLevel* L = p->lev[sc->level].get();
+  cudaStream_t s = p->ctx->stream;
+  SchwarzArgs a;
+  a.N = L->N;
+  a.Ex = L->Ex;
+  a.Ey = L->Ey;
+  a.Ez = L->Ez;
+  a.S = sc->S.p;
+  a.lam = sc->lam.p;
+  a.sidx = sc->sidx.p;
+  a.r = r;
+  a.Lout = sc->Lout.p;
+  a.ras = p->smoother == 2;
+  sem_schwarz_local(a, s);
+  if (a.ras) {
+    SemArgs b = L->args();
+    b.lvec = sc->Lout.p;
+    b.y = out;
+    L->run(SEM_LVEC, EPI_STORE, b);
+    launch_mul(L->len, sc->wmult.p, out, s);
+  } else {
+    sem_asm_gather(a, out, s);
+  }
+}
+
 void pmg_smooth(cmg_pmg* p, int l, const cmg_cheb_config& cfg, std::size_t order, const double* b,
                 double* x, bool xz) {
-  chebyshev_smooth(p->lev[l].get(), p->invd[l]->p, cfg, order, b, x, xz);
+  if (p->smoother == 0) chebyshev_smooth(p->lev[l].get(), p->invd[l]->p, cfg, order, b, x, xz);
+  else chebyshev_smooth_S(p->lev[l].get(), schwarz_apply, p->sch[l].get(), cfg, order, b, x, xz);
 }
 
 // multigrid.hpp:69-90, recursively over the p-levels
@@ -621,7 +731,7 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
     for (int l = 1; l < nlevels; ++l)
       if (orders[l] >= orders[l - 1]) fail(CMG_EINVAL, "pmg: orders must decrease");
     if (orders[nlevels - 1] != 1) fail(CMG_EINVAL, "pmg: the coarsest level must be p=1");
-    if (smoother != 0) fail(CMG_EINVAL, "pmg: Schwarz smoothers are not built yet");
+    if (smoother < 0 || smoother > 2) fail(CMG_EINVAL, "pmg: smoother must be 0 (Jacobi), 1 (ASM) or 2 (RAS)");
     auto p = std::make_unique<cmg_pmg>();
     p->ctx = ctx;
     p->nlevels = nlevels;
@@ -692,10 +802,16 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
       b->alloc(C->len);
       b->zero(s);
     }
-    // lambda_tilde per smoothed level (smoothers.hpp:61-79 with S = invD)
+    // lambda_tilde per smoothed level (smoothers.hpp:61-79; S = invD or the Schwarz operator)
     p->lambda.assign(nlevels, 0.0);
     for (int l = 0; l + 1 < nlevels; ++l) {
-      p->lambda[l] = estimate_lambda_max(p->lev[l].get(), p->invd[l]->p, eigen_iterations, eigen_seed);
+      if (smoother == 0) {
+        p->lambda[l] = estimate_lambda_max(p->lev[l].get(), p->invd[l]->p, eigen_iterations, eigen_seed);
+      } else {
+        schwarz_setup(p.get(), l);
+        p->lambda[l] = estimate_lambda_max_S(p->lev[l].get(), schwarz_apply, p->sch[l].get(), eigen_iterations,
+                                             eigen_seed);
+      }
       p->lev[l]->count = 0;
     }
     ctx->sync();
@@ -721,8 +837,9 @@ int cmg_pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
 }
 int cmg_pmg_schwarz_apply(cmg_pmg* p, int level, const double* r, double* out) {
   return guard([&] {
-    (void)p; (void)level; (void)r; (void)out;
-    fail(CMG_EINVAL, "pmg: Schwarz smoothers are not built yet");
+    if (p->smoother == 0 || level < 0 || level >= static_cast<int>(p->sch.size()) || !p->sch[level])
+      fail(CMG_EINVAL, "pmg: no Schwarz smoother on this level");
+    schwarz_apply(p->sch[level].get(), r, out);
   });
 }
 int cmg_pmg_smooth(cmg_pmg* p, int level, const cmg_cheb_config* cfg, size_t order, const double* b,

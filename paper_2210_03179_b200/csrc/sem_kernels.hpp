@@ -114,16 +114,18 @@ void sem_layer_finalize(const double* gathered, int nv, const int* layers_per_ra
                         double* out, int do_sqrt, cudaStream_t s);
 
 // Schwarz (ASM/RAS) with FDM local solves
+// single-rank (the Schwarz configs are 1-GPU, BASELINE configs[2])
 struct SchwarzArgs {
-  int N, Ex, Ey, Ezl, Ez, z0;
-  const double* S;    // [E][3][pb*pb]   (column eigenvectors, S^T B S = I)
-  const double* lam;  // [E][3][pb]
-  const double* r;    // input residual (slots)
-  const double* halo_lo;  // [Ex*Ey*N*N*2]: two top layers (c=N-1, N-2) of the layer below
-  const double* halo_hi;  // [Ex*Ey*N*N*2]? (c=0,1) of the layer above
-  double* Lout;       // output local (ras: (N+1)^3 per element; asm: (N+3)^3)
-  int ras;
+  int N = 7, Ex = 1, Ey = 1, Ez = 1;
+  const double* S = nullptr;    // unique 1D eigenbases [nu][pb*pb] (columns, S^T B S = I)
+  const double* lam = nullptr;  // [nu][pb]
+  const int* sidx = nullptr;    // [E][3] index of each element's x/y/z basis
+  const double* r = nullptr;    // input residual (slots)
+  double* Lout = nullptr;       // local solutions (ras: (N+1)^3 per element; asm: (N+3)^3)
+  int ras = 1;
 };
 void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s);
+// ASM: y = W sum_e R_e^T Lout_e  (W = 1/number of covering subdomains)
+void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s);
 
 }  // namespace cmg

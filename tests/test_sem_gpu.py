@@ -146,6 +146,41 @@ def test_kershaw_solves(cm, sem, eps, kpre, kpost, htol):
     assert np.linalg.norm(P.A.to_canonical(x) - oref.x) <= htol * np.linalg.norm(oref.x)
 
 
+@pytest.mark.parametrize("ras", [0, 1])
+@pytest.mark.parametrize("N,geo", [(7, 0), (3, 0), (7, 1)])
+def test_schwarz_apply(sem, ras, N, geo):
+    """Chebyshev-Schwarz smoother S_ASM / S_RAS vs the oracle."""
+    d = sem.SemDesc(N, 3, 2, 3, geometry=geo, eps=0.3)
+    orders = (N, 1) if N == 3 else (N, 3, 1)
+    P = sem.PMGHierarchy(d, orders, smoother=sem.RAS if ras else sem.ASM)
+    o = ob.OracleSem(N, 3, 2, 3, geo, 0.3)
+    r = ob.random_vector(o.n, 9)
+    out = P.A.new_vector()
+    from paper_2210_03179_b200 import _lib
+    import ctypes as C
+
+    _lib.check(_lib.lib.cmg_pmg_schwarz_apply(P.h, 0, C.c_void_p(P.A.from_canonical(r).data_ptr()),
+                                              C.c_void_p(out.data_ptr())))
+    assert rel(P.A.to_canonical(out), o.schwarz(r, ras)) <= 1e-11
+
+
+@pytest.mark.parametrize("smoother,fam,kpre,kpost", [(2, 2, 2, 0), (1, 2, 2, 0), (2, 0, 1, 1), (1, 3, 2, 0)])
+def test_schwarz_pmg_solves(cm, sem, smoother, fam, kpre, kpost):
+    """BASELINE configs[2] shape: Chebyshev-ASM/RAS p-MG(7,3,1) PGMRES (non-symmetric smoother)."""
+    ex, ey, ez = 3, 3, 2
+    P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez), (7, 3, 1), smoother=smoother)
+    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, smoother=smoother)
+    for l in (0, 1):
+        assert abs(P.lambda_tilde[l] - o.lambda_tilde[l]) <= 1e-10 * o.lambda_tilde[l]
+    b = o.sem(0).rhs()
+    oref = o.solve(1, fam, kpre, kpost, b, tol=1e-8)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
+    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
+    assert (rep.iterations, rep.fine_matvecs) == (oref.iterations, oref.fine_matvecs)
+    h, hr = np.array(rep.residual_history), np.array(oref.history)
+    assert np.max(np.abs(h - hr)) <= TOL * hr[0]
+
+
 def test_determinism(cm, sem):
     d = sem.SemDesc(7, 3, 3, 3)
     P = sem.PMGHierarchy(d, (7, 3, 1))
