@@ -15,9 +15,9 @@ OBJ = build/obj
 LIB = paper_2210_03179_b200/lib/libchebmg_b200.so
 
 CU_EXACT = $(SRC)/k_blas.cu $(SRC)/k_fd.cu           # --fmad=false (reference rounding)
-CU_FAST  = $(wildcard $(SRC)/k_sem*.cu)              # FMA on (no reference bits to match)
+CU_FAST  = $(wildcard $(SRC)/k_sem*.cu $(SRC)/k_schwarz*.cu)  # FMA on (no reference bits to match)
 CPP      = $(SRC)/capi.cpp $(SRC)/host_setup.cpp $(wildcard $(SRC)/sem*.cpp) $(wildcard $(SRC)/comm*.cpp)
-HDR      = $(wildcard $(SRC)/*.hpp) include/chebmg_b200.h
+HDR      = $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh) include/chebmg_b200.h
 
 OBJS = $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_EXACT) $(CU_FAST)) \
        $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CPP))
@@ -42,7 +42,7 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(HDR)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static $(NCCL_LINK) -lpthread -ldl -lrt
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static $(NCCL_LINK) -lpthread -ldl -lrt -Xlinker --no-undefined
 
 oracle:
 	$(MAKE) -C oracle
