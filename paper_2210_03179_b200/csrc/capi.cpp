@@ -78,8 +78,9 @@ struct FdOp final : cmg_op {
     if (!xz) ++count;
   }
   void cheb4_step(double beta, double c1, double c2, bool xz, const double* invd,
-                  const double* r_in, double* x, double* r, const double* d, double* d_out) override {
-    fd_cheb4_step(g, beta, c1, c2, xz, invd, r_in, x, r, d, d_out, ctx->stream);
+                  const double* r_in, double* x, double* r, const double* d, double* d_out,
+                  double beta_last) override {
+    fd_cheb4_step(g, beta, c1, c2, xz, invd, r_in, x, r, d, d_out, beta_last, ctx->stream);
     ++count;
   }
   void cheb1_init(const double* b, const double* x, bool xz, const double* invd, double theta,
@@ -88,8 +89,8 @@ struct FdOp final : cmg_op {
     if (!xz) ++count;
   }
   void cheb1_step(double c1, double c2, bool xz, const double* invd, double* x, double* z,
-                  const double* d, double* d_out) override {
-    fd_cheb1_step(g, c1, c2, xz, invd, x, z, d, d_out, ctx->stream);
+                  const double* d, double* d_out, double beta_last) override {
+    fd_cheb1_step(g, c1, c2, xz, invd, x, z, d, d_out, beta_last, ctx->stream);
     ++count;
   }
 };
@@ -108,9 +109,10 @@ void cmg_op::cheb4_init(const double* b, const double* x, bool xz, const double*
 }
 
 void cmg_op::cheb4_step(double beta, double c1, double c2, bool xz, const double* invd,
-                        const double* r_in, double* x, double* r, const double* d, double* d_out) {
+                        const double* r_in, double* x, double* r, const double* d, double* d_out,
+                        double beta_last) {
   (void)beta; (void)c1; (void)c2; (void)xz; (void)invd; (void)r_in; (void)x; (void)r; (void)d;
-  (void)d_out;
+  (void)d_out; (void)beta_last;
   fail(CMG_ERUNTIME, "operator has no fused 4th-kind step");
 }
 void cmg_op::cheb1_init(const double* b, const double* x, bool xz, const double* invd,
@@ -119,8 +121,8 @@ void cmg_op::cheb1_init(const double* b, const double* x, bool xz, const double*
   fail(CMG_ERUNTIME, "operator has no fused 1st-kind init");
 }
 void cmg_op::cheb1_step(double c1, double c2, bool xz, const double* invd, double* x, double* z,
-                        const double* d, double* d_out) {
-  (void)c1; (void)c2; (void)xz; (void)invd; (void)x; (void)z; (void)d; (void)d_out;
+                        const double* d, double* d_out, double beta_last) {
+  (void)c1; (void)c2; (void)xz; (void)invd; (void)x; (void)z; (void)d; (void)d_out; (void)beta_last;
   fail(CMG_ERUNTIME, "operator has no fused 1st-kind step");
 }
 
@@ -159,17 +161,18 @@ void chebyshev_smooth(cmg_op* A, const double* invd, const cmg_cheb_config& cfg,
     const double inv_lmax = 1.0 / lmax;
     A->cheb4_init(b, x, x_is_zero, invd, (4.0 / 3.0) * inv_lmax, r, d);
     bool xz = x_is_zero;
+    const double bk = beta ? beta[order - 1] : 1.0;
     for (std::size_t it = 1; it < order; ++it) {
       const double bi = beta ? beta[it - 1] : 1.0;
       const double fi = static_cast<double>(it);
       const double c1 = (2.0 * fi - 1.0) / (2.0 * fi + 3.0);
       const double c2 = (8.0 * fi + 4.0) / (2.0 * fi + 3.0) * inv_lmax;
-      A->cheb4_step(bi, c1, c2, xz, invd, r, x, r, d, d2);
+      // the last step also applies the final x += beta_k d' (same rounding order)
+      A->cheb4_step(bi, c1, c2, xz, invd, r, x, r, d, d2, it + 1 == order ? bk : 0.0);
       std::swap(d, d2);
       xz = false;
     }
-    vec_final_update(A->len, beta ? beta[order - 1] : 1.0, xz, d, x, A->ctx->stream);
-    g_kernel_launches.fetch_add(0);
+    if (order == 1) vec_final_update(A->len, bk, xz, d, x, A->ctx->stream);
   } else {  // smoothers.hpp:95-120
     const double lmin = cfg.lambda_min_multiplier * cfg.lambda_tilde;
     const double theta = 0.5 * (lmax + lmin);
@@ -182,12 +185,12 @@ void chebyshev_smooth(cmg_op* A, const double* invd, const cmg_cheb_config& cfg,
       const double rho = 1.0 / (2.0 * sigma - rho_prev);
       const double c1 = rho * rho_prev;
       const double c2 = 2.0 * rho / delta;
-      A->cheb1_step(c1, c2, xz, invd, x, r, d, d2);
+      A->cheb1_step(c1, c2, xz, invd, x, r, d, d2, it + 1 == order ? 1.0 : 0.0);
       std::swap(d, d2);
       rho_prev = rho;
       xz = false;
     }
-    vec_final_update(A->len, 1.0, xz, d, x, A->ctx->stream);
+    if (order == 1) vec_final_update(A->len, 1.0, xz, d, x, A->ctx->stream);
   }
   // keep the op's canonical scratch pointers stable for the next call
   if (d != A->s_d.p) std::swap(A->s_d.p, A->s_d2.p);

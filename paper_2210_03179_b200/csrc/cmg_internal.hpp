@@ -119,13 +119,14 @@ void fd_cheb4_init(const FdGrid& g, const double* b, const double* x, bool x_is_
 // one 4th-kind step: x += beta d ; r -= A d ; d_out = c1 d + c2 invD r
 void fd_cheb4_step(const FdGrid& g, double beta, double c1, double c2, bool x_zero,
                    const double* invd, const double* r_in, double* x, double* r, const double* d,
-                   double* d_out, cudaStream_t s);
+                   double* d_out, double beta_last, cudaStream_t s);
 // 1st-kind init: z = invD (b - A x) ; d = z / theta
 void fd_cheb1_init(const FdGrid& g, const double* b, const double* x, bool x_is_zero,
                    const double* invd, double theta, double* z, double* d, cudaStream_t s);
 // one 1st-kind step: x += d ; z -= invD A d ; d_out = c1 d + c2 z
 void fd_cheb1_step(const FdGrid& g, double c1, double c2, bool x_zero, const double* invd,
-                   double* x, double* z, const double* d, double* d_out, cudaStream_t s);
+                   double* x, double* z, const double* d, double* d_out, double beta_last,
+                   cudaStream_t s);
 // x += beta d  (or x = beta d when x_zero)
 void vec_final_update(std::size_t n, double beta, bool x_zero, const double* d, double* x,
                       cudaStream_t s);

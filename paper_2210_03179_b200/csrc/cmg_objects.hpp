@@ -127,12 +127,15 @@ struct cmg_op {
   // unfused kernels; FD and SEM operators override with one fused kernel.
   virtual void cheb4_init(const double* b, const double* x, bool x_is_zero, const double* invd,
                           double c0, double* r, double* d);
+  // beta_last > 0 marks the LAST step of a sweep: the final x += beta_k d'
+  // (smoothers.hpp:146-147 / :119) is fused in and r, d' are not written back.
   virtual void cheb4_step(double beta, double c1, double c2, bool x_zero, const double* invd,
-                          const double* r_in, double* x, double* r, const double* d, double* d_out);
+                          const double* r_in, double* x, double* r, const double* d, double* d_out,
+                          double beta_last = 0.0);
   virtual void cheb1_init(const double* b, const double* x, bool x_is_zero, const double* invd,
                           double theta, double* z, double* d);
   virtual void cheb1_step(double c1, double c2, bool x_zero, const double* invd, double* x,
-                          double* z, const double* d, double* d_out);
+                          double* z, const double* d, double* d_out, double beta_last = 0.0);
   // Inner products over the operator's vector space (distributed ops reduce
   // across ranks); results land in device memory.
   virtual void dot(const double* a, const double* b, double* out_dev) {

@@ -79,17 +79,23 @@ __global__ void k_fd_cheb4_step(int m, double ihx2, double ihy2, double beta, do
                                 int x_zero, const double* __restrict__ invd,
                                 const double* __restrict__ r_in, double* __restrict__ x,
                                 double* __restrict__ r, const double* __restrict__ d,
-                                double* __restrict__ d_out) {
+                                double* __restrict__ d_out, double beta_last) {
   const int ix = blockIdx.x * BX + threadIdx.x, iy = blockIdx.y * BY + threadIdx.y;
   if (ix >= m || iy >= m) return;
   const long id = (long)iy * m + ix;
   const double c = 2.0 * (ihx2 + ihy2);
   const double dv = d[id];
-  x[id] = x_zero ? beta * dv : x[id] + beta * dv;
+  const double xv = x_zero ? beta * dv : x[id] + beta * dv;
   const double t = stencil(d, ix, iy, m, c, ihx2, ihy2);
   const double rv = r_in[id] + -1.0 * t;
-  r[id] = rv;
-  d_out[id] = c1 * dv + c2 * invd[id] * rv;
+  const double dn = c1 * dv + c2 * invd[id] * rv;
+  if (beta_last > 0.0) {  // last step: fused final x += beta_k d (smoothers.hpp:146-147)
+    x[id] = xv + beta_last * dn;
+  } else {
+    x[id] = xv;
+    r[id] = rv;
+    d_out[id] = dn;
+  }
 }
 
 // smoothers.hpp:104-107
@@ -111,17 +117,23 @@ __global__ void k_fd_cheb1_init(int m, double ihx2, double ihy2, const double* _
 __global__ void k_fd_cheb1_step(int m, double ihx2, double ihy2, double c1, double c2, int x_zero,
                                 const double* __restrict__ invd, double* __restrict__ x,
                                 double* __restrict__ z, const double* __restrict__ d,
-                                double* __restrict__ d_out) {
+                                double* __restrict__ d_out, double beta_last) {
   const int ix = blockIdx.x * BX + threadIdx.x, iy = blockIdx.y * BY + threadIdx.y;
   if (ix >= m || iy >= m) return;
   const long id = (long)iy * m + ix;
   const double c = 2.0 * (ihx2 + ihy2);
   const double dv = d[id];
-  x[id] = x_zero ? 1.0 * dv : x[id] + 1.0 * dv;
+  const double xv = x_zero ? 1.0 * dv : x[id] + 1.0 * dv;
   const double t = stencil(d, ix, iy, m, c, ihx2, ihy2);
   const double zv = z[id] - invd[id] * t;
-  z[id] = zv;
-  d_out[id] = c1 * dv + c2 * zv;
+  const double dn = c1 * dv + c2 * zv;
+  if (beta_last > 0.0) {  // last step: fused final x += d (smoothers.hpp:119)
+    x[id] = xv + beta_last * dn;
+  } else {
+    x[id] = xv;
+    z[id] = zv;
+    d_out[id] = dn;
+  }
 }
 
 __global__ void k_final_update(std::size_t n, double beta, int x_zero, const double* __restrict__ d,
@@ -264,9 +276,9 @@ void fd_cheb4_init(const FdGrid& g, const double* b, const double* x, bool x_is_
 
 void fd_cheb4_step(const FdGrid& g, double beta, double c1, double c2, bool x_zero,
                    const double* invd, const double* r_in, double* x, double* r, const double* d,
-                   double* d_out, cudaStream_t s) {
+                   double* d_out, double beta_last, cudaStream_t s) {
   k_fd_cheb4_step<<<grid2d(g.m), dim3(BX, BY), 0, s>>>(g.m, g.ihx2, g.ihy2, beta, c1, c2, x_zero,
-                                                       invd, r_in, x, r, d, d_out);
+                                                       invd, r_in, x, r, d, d_out, beta_last);
   CMG_LAUNCH_CHECK();
 }
 
@@ -278,9 +290,10 @@ void fd_cheb1_init(const FdGrid& g, const double* b, const double* x, bool x_is_
 }
 
 void fd_cheb1_step(const FdGrid& g, double c1, double c2, bool x_zero, const double* invd,
-                   double* x, double* z, const double* d, double* d_out, cudaStream_t s) {
+                   double* x, double* z, const double* d, double* d_out, double beta_last,
+                   cudaStream_t s) {
   k_fd_cheb1_step<<<grid2d(g.m), dim3(BX, BY), 0, s>>>(g.m, g.ihx2, g.ihy2, c1, c2, x_zero, invd,
-                                                       x, z, d, d_out);
+                                                       x, z, d, d_out, beta_last);
   CMG_LAUNCH_CHECK();
 }
 

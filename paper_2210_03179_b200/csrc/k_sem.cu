@@ -107,16 +107,28 @@ __device__ __forceinline__ void epilogue(const SemArgs& A, long slot, double w, 
     A.r[slot] = o0 - w;
   } else if constexpr (EPI == EPI_CHEB4) {
     // smoothers.hpp:138-144: x += beta d ; r -= A d ; d = c1 d + c2 invD r
-    A.x[slot] = A.x_zero ? A.beta * dv : o0 + A.beta * dv;
+    const double xv = A.x_zero ? A.beta * dv : o0 + A.beta * dv;
     const double rv = o1 - w;
-    A.r[slot] = rv;
-    A.d_out[slot] = A.c1 * dv + A.c2 * o2 * rv;
+    const double dn = A.c1 * dv + A.c2 * o2 * rv;
+    if (A.beta_last > 0.0) {  // last step: fused final x += beta_k d (smoothers.hpp:146-147)
+      A.x[slot] = xv + A.beta_last * dn;
+    } else {
+      A.x[slot] = xv;
+      A.r[slot] = rv;
+      A.d_out[slot] = dn;
+    }
   } else if constexpr (EPI == EPI_CHEB1) {
     // smoothers.hpp:109-118: x += d ; z -= invD A d ; d = c1 d + c2 z
-    A.x[slot] = A.x_zero ? dv : o0 + dv;
+    const double xv = A.x_zero ? dv : o0 + dv;
     const double zv = o1 - o2 * w;
-    A.r[slot] = zv;
-    A.d_out[slot] = A.c1 * dv + A.c2 * zv;
+    const double dn = A.c1 * dv + A.c2 * zv;
+    if (A.beta_last > 0.0) {  // last step: fused final x += d (smoothers.hpp:119)
+      A.x[slot] = xv + A.beta_last * dn;
+    } else {
+      A.x[slot] = xv;
+      A.r[slot] = zv;
+      A.d_out[slot] = dn;
+    }
   } else if constexpr (EPI == EPI_CHEB4_INIT) {
     const double rv = o0 - w;
     A.r[slot] = rv;
@@ -881,9 +893,6 @@ __device__ __forceinline__ void k2_build_table(K2Table<N>* T, const int* lut) {
 template <int N, int EPI>
 __global__ void k_sem_k2(SemArgs A) {
   constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N), NSH = sem_nshared(N);
-  __shared__ K2Table<N> T;
-  k2_build_table<N>(&T, A.lut);
-  __syncthreads();
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long q = tid / NSH;
   const int s = (int)(tid - q * NSH);
@@ -894,12 +903,13 @@ __global__ void k_sem_k2(SemArgs A) {
   sem_shared_abc(N, s, a, b, c);
   // padding (far domain boundary) is not an unknown
   if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
-  const int n = T.cnt[s];
+  const int* tab = A.k2tab + s * 9;  // host-built (sem.cpp), L1-resident
+  const int n = __ldg(tab);
   double vals[8];
 #pragma unroll
   for (int cidx = 0; cidx < 8; ++cidx) {
     if (cidx < n) {
-      const int p = T.ent[s][cidx];
+      const int p = __ldg(tab + 1 + cidx);
       const int li = p & 0xffff, dx = (p >> 16) & 1, dy = (p >> 17) & 1, dz = (p >> 18) & 1;
       if (ez + dz >= A.Ezl) {
         // halo: k=0 face of the layer above, indexed by (ex', ey', i', j')

@@ -96,7 +96,7 @@ struct SemLevel final : cmg_op {
   int nshell = 0, nshared = 0;
   DBuf G, Dm, xi, w, shell, halo_lo, halo_send, contrib_hi, contrib_send, diagv, mask, Lrhs;
   DBuf lpart, lout, lgath;
-  IBuf lut, shared, lpr;
+  IBuf lut, shared, lpr, k2tab;
   std::vector<int> lpr_h;
 
   SemLevel(cmg_ctx* c, const cmg_sem_desc& d) {
@@ -135,6 +135,26 @@ struct SemLevel final : cmg_op {
     nshared = static_cast<int>(sh_h.size());
     lut.upload(lut_h);
     shared.upload(sh_h);
+    // K2 contributor table: per shared slot s (interior-first order) its <= 8
+    // contributions (shell index | dx<<16 | dy<<17 | dz<<18) in fixed (dz,dy,dx) order
+    {
+      const int nsh = sem_nshared(N);
+      std::vector<int> tab(static_cast<std::size_t>(nsh) * 9, 0);
+      for (int s2 = 0; s2 < nsh; ++s2) {
+        int a2, b2, c2;
+        sem_shared_abc(N, s2, a2, b2, c2);
+        const int i = a2 + 1, j = b2 + 1, k = c2 + 1;
+        int cnt = 0;
+        for (int dz = 0; dz < (k == N ? 2 : 1); ++dz)
+          for (int dy = 0; dy < (j == N ? 2 : 1); ++dy)
+            for (int dx = 0; dx < (i == N ? 2 : 1); ++dx) {
+              const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
+              tab[s2 * 9 + 1 + cnt++] = lut_h[(lk * N1 + lj) * N1 + li] | (dx << 16) | (dy << 17) | (dz << 18);
+            }
+        tab[s2 * 9] = cnt;
+      }
+      k2tab.upload(tab);
+    }
     // basis
     std::vector<double> xih(N1), wh(N1), Dh(N1 * N1);
     host_gll(N, xih.data(), wh.data());
@@ -204,6 +224,7 @@ struct SemLevel final : cmg_op {
     a.shared = shared.p;
     a.nshared = nshared;
     a.nshell = nshell;
+    a.k2tab = k2tab.p;
     a.shell = shell.p;
     a.halo_lo = halo_lo.p;
     a.contrib_hi = contrib_hi.p;
@@ -277,7 +298,8 @@ struct SemLevel final : cmg_op {
     ++count;
   }
   void cheb4_step(double beta, double c1, double c2, bool xz, const double* invd,
-                  const double* r_in, double* x, double* r, const double* d, double* d_out) override {
+                  const double* r_in, double* x, double* r, const double* d, double* d_out,
+                  double beta_last) override {
     SemArgs a = args();
     a.u = d;
     a.d = d;
@@ -289,6 +311,7 @@ struct SemLevel final : cmg_op {
     a.beta = beta;
     a.c1 = c1;
     a.c2 = c2;
+    a.beta_last = beta_last;
     a.x_zero = xz ? 1 : 0;
     run(SEM_AX, EPI_CHEB4, a);
     ++count;
@@ -310,7 +333,7 @@ struct SemLevel final : cmg_op {
     ++count;
   }
   void cheb1_step(double c1, double c2, bool xz, const double* invd, double* x, double* z,
-                  const double* d, double* d_out) override {
+                  const double* d, double* d_out, double beta_last) override {
     SemArgs a = args();
     a.u = d;
     a.d = d;
@@ -320,6 +343,7 @@ struct SemLevel final : cmg_op {
     a.invd = invd;
     a.c1 = c1;
     a.c2 = c2;
+    a.beta_last = beta_last;
     a.x_zero = xz ? 1 : 0;
     run(SEM_AX, EPI_CHEB1, a);
     ++count;

@@ -57,7 +57,9 @@ struct SemArgs {
   double* d_out = nullptr;
   const double* invd = nullptr;
   double beta = 1, c1 = 0, c2 = 0, c0 = 0, theta = 1;
+  double beta_last = 0;  // > 0: last sweep step, final x += beta_k d' fused, r/d' not stored
   int x_zero = 0;
+  const int* k2tab = nullptr;  // K2 contributor table [nshared][9] (count + 8 packed entries)
   // element range [e_begin, e_end) processed by this launch (for overlap splits)
   long e_begin = 0, e_end = 0;
 };
