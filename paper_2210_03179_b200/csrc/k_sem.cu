@@ -15,6 +15,8 @@
 // into shared memory with TMA bulk copies (cp.async.bulk + mbarrier) while
 // all threads gather the input vector; w_r, w_s, w_t then overwrite the
 // factors in place, so a block needs ~34 KB and six blocks share an SM.
+#include <cstdlib>
+
 #include "sem_kernels.hpp"
 #include "sem_layout.hpp"
 
@@ -944,14 +946,22 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
   if constexpr (MODE == SEM_AX && N >= 5 && (N + 1) % 2 == 0) {
-    // line-contraction kernel, two threads per line (v5)
+    // line-contraction kernel (k_sem_k1.cuh): KS threads per line; 4 when N+1 allows
     constexpr std::size_t smem = K3Smem<N, EPI>::bytes;
-    static bool configured = false;
-    if (!configured) {
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      configured = true;
+    static int ks = 0;
+    if (ks == 0) {
+      const char* env = std::getenv("CMG_K1_SPLIT");  // tuning knob: 2 or 4
+      ks = ((N + 1) % 4 == 0) ? (env && std::atoi(env) == 2 ? 2 : 4) : 2;
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if constexpr ((N + 1) % 4 == 0)
+        CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    k_sem_k1_lines<N, EPI><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
+    if constexpr ((N + 1) % 4 == 0) {
+      if (ks == 4) k_sem_k1_lines<N, EPI, 4><<<(unsigned)ne, (N + 1) * (N + 1) * 4, smem, s>>>(a);
+      else k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
+    } else {
+      k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
+    }
   } else if constexpr (MODE == SEM_AX && N >= 5) {
     // persistent register-blocked line kernel, double-buffered TMA / cp.async prefetch
     constexpr std::size_t smem = K4Smem<N, EPI>::bytes;

@@ -17,11 +17,12 @@
 //   4. divergence (r rows, s columns accumulate, t on the column) ->
 //      epilogue: interior nodes finished in place, shell nodes to K2.
 
-template <int N, int EPI>
+template <int N, int EPI, int KS>
 struct K1L {
   using S = K3Smem<N, EPI>;
   static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
-  static constexpr int R = N1 + 1, KH = N1 / 2;
+  static constexpr int R = N1 + 1, KH = N1 / KS;
+  static_assert(N1 % KS == 0, "line split must divide N+1");
   __device__ static constexpr int idx(int i, int j, int k) { return ((k * N1 + j) * R + i); }
 
   template <int H>
@@ -164,9 +165,9 @@ struct K1L {
   }
 };
 
-template <int N, int EPI>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_lines(SemArgs A) {
-  using L = K1L<N, EPI>;
+template <int N, int EPI, int KS>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs A) {
+  using L = K1L<N, EPI, KS>;
   using S = typename L::S;
   constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP, KH = L::KH;
   extern __shared__ __align__(128) double sm[];
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_lines(SemArgs 
   const int t = threadIdx.x;
   const long e = A.e_begin + blockIdx.x;
   const int line = t % (N1 * N1);
-  const bool h0 = t < N1 * N1;  // warp-uniform half selector
+  const int h = t / (N1 * N1);  // line part: warp-uniform for N1*N1 a multiple of 32
   const int ta = line % N1, tb = line / N1;
   if (t == 0) {  // 1. TMA
     const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
@@ -196,23 +197,28 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_lines(SemArgs 
       }
     }
   }
-  if (h0) L::template gather<0>(A, su, ta, tb, e);
-  else L::template gather<1>(A, su, ta, tb, e);
-  __syncthreads();
   double wt[KH], dvh[KH];
-  if (h0) L::template gradient<0>(su, sr, ss, ta, tb, wt, dvh);
-  else L::template gradient<1>(su, sr, ss, ta, tb, wt, dvh);
+// run a phase on this thread's line part with a compile-time part index (h < KS <= 4)
+#define ON_PART(fn, ...)                                   \
+  do {                                                     \
+    switch (h) {                                           \
+      case 0: L::template fn<0>(__VA_ARGS__); break;       \
+      case 1: L::template fn<1 % KS>(__VA_ARGS__); break;  \
+      case 2: L::template fn<2 % KS>(__VA_ARGS__); break;  \
+      default: L::template fn<3 % KS>(__VA_ARGS__); break; \
+    }                                                      \
+  } while (0)
+  ON_PART(gather, A, su, ta, tb, e);
+  __syncthreads();
+  ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
   __syncthreads();
   mbar_wait(bar, 0);
-  if (h0) L::template geometry<0>(sG, sr, ss, ta, tb, wt);
-  else L::template geometry<1>(sG, sr, ss, ta, tb, wt);
+  ON_PART(geometry, sG, sr, ss, ta, tb, wt);
   __syncthreads();
-  if (h0) L::template div_r<0>(sr, su, ta, tb);
-  else L::template div_r<1>(sr, su, ta, tb);
+  ON_PART(div_r, sr, su, ta, tb);
   __syncthreads();
-  if (h0) L::template div_s<0>(ss, su, sr, ta, tb, wt);
-  else L::template div_s<1>(ss, su, sr, ta, tb, wt);
+  ON_PART(div_s, ss, su, sr, ta, tb, wt);
   __syncthreads();
-  if (h0) L::template finish<0>(A, su, sr, so, ta, tb, e, dvh);
-  else L::template finish<1>(A, su, sr, so, ta, tb, e, dvh);
+  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
+#undef ON_PART
 }
