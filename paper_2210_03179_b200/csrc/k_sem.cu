@@ -946,12 +946,13 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
   if constexpr (MODE == SEM_AX && N >= 5 && (N + 1) % 2 == 0) {
-    // line-contraction kernel (k_sem_k1.cuh): KS threads per line; 4 when N+1 allows
+    // line-contraction kernel (k_sem_k1.cuh): KS threads per line.  KS=2 measured
+    // 31.8 vs 31.0 GDOF-step/s for KS=4 at E=64^3 (tools/ab_split.sh); 4 kept as a knob
     constexpr std::size_t smem = K3Smem<N, EPI>::bytes;
     static int ks = 0;
     if (ks == 0) {
       const char* env = std::getenv("CMG_K1_SPLIT");  // tuning knob: 2 or 4
-      ks = ((N + 1) % 4 == 0) ? (env && std::atoi(env) == 2 ? 2 : 4) : 2;
+      ks = ((N + 1) % 4 == 0) ? (env && std::atoi(env) == 4 ? 4 : 2) : 2;
       CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if constexpr ((N + 1) % 4 == 0)
         CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
