@@ -9,12 +9,10 @@
 // interior-first slot order that makes both kernels' vector traffic
 // contiguous per element.
 //
-// K1 (element kernel, AX mode): one element per block, (N+1)^2 x KS threads
-// ((i,j) column x k-half).  A single thread streams the element's geometric
-// factors (24.6 KB at N=7) and the interior blocks of the epilogue operands
-// into shared memory with TMA bulk copies (cp.async.bulk + mbarrier) while
-// all threads gather the input vector; w_r, w_s, w_t then overwrite the
-// factors in place, so a block needs ~34 KB and six blocks share an SM.
+// K1 (element kernel, AX mode) for the high orders is k_sem_k1.cuh (line
+// contractions with the GLL matrix in constant memory, TMA-staged geometric
+// factors and epilogue operands); the low orders (coarse p-levels) use
+// k_sem_k1_ax below (several elements per block, k-split columns).
 #include <cstdlib>
 
 #include "sem_kernels.hpp"
@@ -271,7 +269,7 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
   }
 }
 
-// ---------------------------------------------------------------- K1 v3 (AX mode, register-blocked)
+// ---------------------------------------------------------------- K1 (AX mode, line contractions)
 // GLL derivative matrices per order in constant memory: with compile-time
 // indices every D entry becomes a DFMA constant-bank operand (no LDS).
 __constant__ double c_D[8][64];
@@ -293,551 +291,6 @@ struct K3Smem {
   static constexpr std::size_t bar_off = (s_off + NPP + 1) & ~(std::size_t)1;
   static constexpr std::size_t bytes = (bar_off + 1) * sizeof(double);
 };
-
-template <int N, int EPI>
-__global__ void __launch_bounds__((N + 1) * (N + 1)) k_sem_k1_v3(SemArgs A) {
-  using S = K3Smem<N, EPI>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
-  constexpr int R = N1 + 1;  // padded row length
-#define IDX(i, j, k) (((k) * N1 + (j)) * R + (i))
-#define CD(a, b) c_D[N][(a) * N1 + (b)]
-  extern __shared__ __align__(128) double sm[];
-  double* sG = sm + S::g_off;
-  double* so = sm + S::o_off;
-  double* su = sm + S::u_off;
-  double* sr = sm + S::r_off;
-  double* ss = sm + S::s_off;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
-  const int t = threadIdx.x;
-  const int ta = t % N1, tb = t / N1;  // line coordinates
-  const long e = A.e_begin + blockIdx.x;
-  // 1. TMA: geometric factors + interior operand blocks
-  if (t == 0) {
-    const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
-    unsigned bytes = 6 * NP * sizeof(double);
-    if constexpr (NOPS > 0 && sem_nint(N) > 0) bytes += (NOPS - (skip_x ? 1 : 0)) * NIP * 8;
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(sG, A.G + e * 6 * NP, 6 * NP * sizeof(double), bar);
-    if constexpr (NOPS > 0 && sem_nint(N) > 0) {
-#pragma unroll
-      for (int op = 0; op < NOPS; ++op) {
-        if (op == 0 && skip_x) continue;
-        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * NOS, NIP * 8, bar);
-      }
-    }
-  }
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-  // 2. gather: thread (i,j) = (ta,tb) owns the k-column; keep it in registers too
-  double uc[N1];
-  {
-    const int i = ta, j = tb;
-    int oex = 0, oey = 0;
-    const int ax = owner1d<N>(ex, i, A.Ex, oex);
-    const int ay = owner1d<N>(ey, j, A.Ey, oey);
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      double v = 0.0;
-      if (ax >= 0 && ay >= 0) {
-        int oez = 0;
-        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
-        if (az >= 0) {
-          const int lz = oez - A.z0;
-          if (lz < 0)
-            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
-          else
-            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS + sem_pos(N, ax, ay, az)];
-        }
-      }
-      uc[k] = v;
-      su[IDX(i, j, k)] = v;
-    }
-  }
-  __syncthreads();
-  // 3. gradient: u_r along rows (j,k)=(ta,tb); u_s along columns (i,k)=(ta,tb); u_t in registers
-  {
-    double l[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(m, ta, tb)];
-#pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(i, m) * l[m];
-      sr[IDX(i, ta, tb)] = v;
-    }
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, m, tb)];
-#pragma unroll
-    for (int j = 0; j < N1; ++j) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(j, m) * l[m];
-      ss[IDX(ta, j, tb)] = v;
-    }
-  }
-  double wt[N1];
-#pragma unroll
-  for (int k = 0; k < N1; ++k) {
-    double v = 0.0;
-#pragma unroll
-    for (int m = 0; m < N1; ++m) v += CD(k, m) * uc[m];
-    wt[k] = v;  // u_t for now
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  // 4. geometric factors at the thread's (i,j) column: w = G grad u
-  {
-    const int i = ta, j = tb;
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      const int l = (k * N1 + j) * N1 + i;
-      const double ur = sr[IDX(i, j, k)], us = ss[IDX(i, j, k)], ut = wt[k];
-      const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
-      const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
-      sr[IDX(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
-      ss[IDX(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
-      wt[k] = g2 * ur + g4 * us + g5 * ut;
-    }
-  }
-  __syncthreads();
-  // 5. divergence: D^T along rows into su, then columns accumulate, then k in registers
-  {
-    double l[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = sr[IDX(m, ta, tb)];
-#pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, i) * l[m];
-      su[IDX(i, ta, tb)] = v;
-    }
-  }
-  __syncthreads();
-  {
-    double l[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = ss[IDX(ta, m, tb)];
-#pragma unroll
-    for (int j = 0; j < N1; ++j) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, j) * l[m];
-      su[IDX(ta, j, tb)] += v;
-    }
-  }
-  __syncthreads();
-  // 6. t-divergence + epilogue on the (i,j) column
-  const int i = ta, j = tb;
-  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
-#pragma unroll
-  for (int k = 0; k < N1; ++k) {
-    double v = 0.0;
-#pragma unroll
-    for (int m = 0; m < N1; ++m) v += CD(m, k) * wt[m];
-    v += su[IDX(i, j, k)];
-    if (ij_interior && k >= 1 && k < N) {
-      const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
-      double o0 = 0.0, o1 = 0.0, o2 = 0.0;
-      if constexpr (NOPS > 0) o0 = so[p];
-      if constexpr (NOPS > 1) o1 = so[NIP + p];
-      if constexpr (NOPS > 2) o2 = so[2 * NIP + p];
-      epilogue<EPI>(A, e * NOS + p, v, uc[k], o0, o1, o2);
-    } else {
-      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
-    }
-  }
-#undef IDX
-#undef CD
-}
-
-// ---------------------------------------------------------------- K1 v4 (persistent, double-buffered)
-// Same line-blocked math as v3, but each block loops over elements
-// e = blockIdx.x + it*gridDim.x and, while computing element it, already
-// streams element it+1: geometric factors + interior operand blocks by TMA
-// (mbarrier per buffer) and the gathered input by cp.async (LDGSTS).  Memory
-// parallelism comes from the copy engines, not from resident warps.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int NLEFT>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NLEFT) : "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int N, int EPI>
-struct K4Smem {
-  static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NPP = N1 * N1 * (N1 + 1);
-  static constexpr int NOPS = EpiOps<EPI>::n, NIP = SemC<N>::NINT_PAD;
-  static constexpr std::size_t buf = (std::size_t)6 * NP + (std::size_t)NOPS * NIP + NPP;  // G | ops | u
-  static constexpr std::size_t buf_pad = (buf + 1) & ~(std::size_t)1;
-  static constexpr std::size_t r_off = 2 * buf_pad;  // [NPP] u_r -> w_r -> v
-  static constexpr std::size_t s_off = r_off + NPP;  // [NPP] u_s -> w_s
-  static constexpr std::size_t bar_off = (s_off + NPP + 1) & ~(std::size_t)1;  // 2 mbarriers
-  static constexpr std::size_t bytes = (bar_off + 2) * sizeof(double);
-};
-
-template <int N, int EPI>
-__device__ __forceinline__ void k4_prefetch(const SemArgs& A, long e, double* buf, unsigned long long* bar) {
-  using S = K4Smem<N, EPI>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
-  constexpr int R = N1 + 1;
-  double* sG = buf;
-  double* so = buf + 6 * NP;
-  double* su = so + NOPS * NIP;
-  const int t = threadIdx.x;
-  if (t == 0) {
-    const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
-    unsigned bytes = 6 * NP * sizeof(double);
-    if constexpr (NOPS > 0 && sem_nint(N) > 0) bytes += (NOPS - (skip_x ? 1 : 0)) * NIP * 8;
-    fence_proxy_async();
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(sG, A.G + e * 6 * NP, 6 * NP * sizeof(double), bar);
-    if constexpr (NOPS > 0 && sem_nint(N) > 0) {
-#pragma unroll
-      for (int op = 0; op < NOPS; ++op) {
-        if (op == 0 && skip_x) continue;
-        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * NOS, NIP * 8, bar);
-      }
-    }
-  }
-  // gather Q u with cp.async (owner slots / halo); Dirichlet zeros stored directly
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-  const int i = t % N1, j = t / N1;
-  int oex = 0, oey = 0;
-  const int ax = owner1d<N>(ex, i, A.Ex, oex);
-  const int ay = owner1d<N>(ey, j, A.Ey, oey);
-#pragma unroll
-  for (int k = 0; k < N1; ++k) {
-    double* dst = su + ((k * N1 + j) * R + i);
-    const double* src = nullptr;
-    if (ax >= 0 && ay >= 0) {
-      int oez = 0;
-      const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
-      if (az >= 0) {
-        const int lz = oez - A.z0;
-        src = lz < 0 ? A.halo_lo + ((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay
-                     : A.u + ((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS + sem_pos(N, ax, ay, az);
-      }
-    }
-    if (src) cp_async8(dst, src);
-    else *dst = 0.0;
-  }
-  cp_async_commit();
-}
-
-template <int N, int EPI>
-__global__ void __launch_bounds__((N + 1) * (N + 1)) k_sem_k1_v4(SemArgs A) {
-  using S = K4Smem<N, EPI>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
-  constexpr int R = N1 + 1;
-#define IDX(i, j, k) (((k) * N1 + (j)) * R + (i))
-#define CD(a, b) c_D[N][(a) * N1 + (b)]
-  extern __shared__ __align__(128) double sm[];
-  double* sr = sm + S::r_off;
-  double* ss = sm + S::s_off;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
-  const int t = threadIdx.x;
-  const int ta = t % N1, tb = t / N1;
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-  }
-  __syncthreads();
-  long e = A.e_begin + blockIdx.x;
-  if (e < A.e_end) k4_prefetch<N, EPI>(A, e, sm, &bars[0]);
-  for (int it = 0; e < A.e_end; ++it, e += gridDim.x) {
-    const int cur = it & 1;
-    double* buf = sm + cur * S::buf_pad;
-    double* sG = buf;
-    double* so = buf + 6 * NP;
-    double* su = so + NOPS * NIP;
-    const long en = e + gridDim.x;
-    if (en < A.e_end) {
-      k4_prefetch<N, EPI>(A, en, sm + (cur ^ 1) * S::buf_pad, &bars[cur ^ 1]);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    // gradient (as v3)
-    double uc[N1];
-#pragma unroll
-    for (int k = 0; k < N1; ++k) uc[k] = su[IDX(ta, tb, k)];
-    {
-      double l[N1];
-#pragma unroll
-      for (int m = 0; m < N1; ++m) l[m] = su[IDX(m, ta, tb)];
-#pragma unroll
-      for (int i = 0; i < N1; ++i) {
-        double v = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) v += CD(i, m) * l[m];
-        sr[IDX(i, ta, tb)] = v;
-      }
-#pragma unroll
-      for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, m, tb)];
-#pragma unroll
-      for (int j = 0; j < N1; ++j) {
-        double v = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) v += CD(j, m) * l[m];
-        ss[IDX(ta, j, tb)] = v;
-      }
-    }
-    double wt[N1];
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(k, m) * uc[m];
-      wt[k] = v;
-    }
-    __syncthreads();
-    mbar_wait(&bars[cur], (it >> 1) & 1);
-    {
-      const int i = ta, j = tb;
-#pragma unroll
-      for (int k = 0; k < N1; ++k) {
-        const int l = (k * N1 + j) * N1 + i;
-        const double ur = sr[IDX(i, j, k)], us = ss[IDX(i, j, k)], ut = wt[k];
-        const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
-        const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
-        sr[IDX(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
-        ss[IDX(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
-        wt[k] = g2 * ur + g4 * us + g5 * ut;
-      }
-    }
-    __syncthreads();
-    // divergence: D^T along rows into su (free since the gradient barrier), columns accumulate
-    {
-      double l[N1];
-#pragma unroll
-      for (int m = 0; m < N1; ++m) l[m] = sr[IDX(m, ta, tb)];
-#pragma unroll
-      for (int i = 0; i < N1; ++i) {
-        double v = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) v += CD(m, i) * l[m];
-        su[IDX(i, ta, tb)] = v;
-      }
-    }
-    __syncthreads();
-    {
-      double l[N1];
-#pragma unroll
-      for (int m = 0; m < N1; ++m) l[m] = ss[IDX(ta, m, tb)];
-#pragma unroll
-      for (int j = 0; j < N1; ++j) {
-        double v = 0.0;
-#pragma unroll
-        for (int m = 0; m < N1; ++m) v += CD(m, j) * l[m];
-        su[IDX(ta, j, tb)] += v;
-      }
-    }
-    __syncthreads();
-    const int i = ta, j = tb;
-    const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, k) * wt[m];
-      v += su[IDX(i, j, k)];
-      if (ij_interior && k >= 1 && k < N) {
-        const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
-        double o0 = 0.0, o1 = 0.0, o2 = 0.0;
-        if constexpr (NOPS > 0) o0 = so[p];
-        if constexpr (NOPS > 1) o1 = so[NIP + p];
-        if constexpr (NOPS > 2) o2 = so[2 * NIP + p];
-        epilogue<EPI>(A, e * NOS + p, v, uc[k], o0, o1, o2);
-      } else {
-        A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
-      }
-    }
-    __syncthreads();  // buffers of this iteration may be refilled by the next prefetch
-  }
-#undef IDX
-#undef CD
-}
-
-// ---------------------------------------------------------------- K1 v5 (line contractions, 2 threads per line)
-// v3's layout (TMA-staged factors/operands, constant-memory D, one shared
-// access per line element) with each line's N+1 outputs split across KS
-// threads: twice the warps of v3 for the same shared memory, ~2 shared loads
-// per output instead of v2's 2(N+1).
-template <int N, int EPI>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * 2) k_sem_k1_v5(SemArgs A) {
-  using S = K3Smem<N, EPI>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
-  constexpr int R = N1 + 1;
-  constexpr int KS = 2, KH = N1 / KS;  // outputs per thread per line
-  static_assert(N1 % KS == 0, "v5 needs an even number of GLL points");
-#define IDX(i, j, k) (((k) * N1 + (j)) * R + (i))
-#define CD(a, b) c_D[N][(a) * N1 + (b)]
-  extern __shared__ __align__(128) double sm[];
-  double* sG = sm + S::g_off;
-  double* so = sm + S::o_off;
-  double* su = sm + S::u_off;
-  double* sr = sm + S::r_off;
-  double* ss = sm + S::s_off;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
-  const int t = threadIdx.x;
-  const int line = t % (N1 * N1), h = t / (N1 * N1);
-  const int ta = line % N1, tb = line / N1;
-  const int o0i = h * KH;  // first output index of this thread within a line
-  const long e = A.e_begin + blockIdx.x;
-  if (t == 0) {
-    const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
-    unsigned bytes = 6 * NP * sizeof(double);
-    if constexpr (NOPS > 0 && sem_nint(N) > 0) bytes += (NOPS - (skip_x ? 1 : 0)) * NIP * 8;
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(sG, A.G + e * 6 * NP, 6 * NP * sizeof(double), bar);
-    if constexpr (NOPS > 0 && sem_nint(N) > 0) {
-#pragma unroll
-      for (int op = 0; op < NOPS; ++op) {
-        if (op == 0 && skip_x) continue;
-        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * NOS, NIP * 8, bar);
-      }
-    }
-  }
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-  // gather: thread (i,j,h) loads k in [h*KH, h*KH+KH)
-  {
-    const int i = ta, j = tb;
-    int oex = 0, oey = 0;
-    const int ax = owner1d<N>(ex, i, A.Ex, oex);
-    const int ay = owner1d<N>(ey, j, A.Ey, oey);
-#pragma unroll
-    for (int kk = 0; kk < KH; ++kk) {
-      const int k = o0i + kk;
-      double v = 0.0;
-      if (ax >= 0 && ay >= 0) {
-        int oez = 0;
-        const int az = owner1d<N>(A.z0 + ez, k, A.Ez, oez);
-        if (az >= 0) {
-          const int lz = oez - A.z0;
-          if (lz < 0)
-            v = A.halo_lo[((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay];
-          else
-            v = A.u[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS + sem_pos(N, ax, ay, az)];
-        }
-      }
-      su[IDX(i, j, k)] = v;
-    }
-  }
-  __syncthreads();
-  // gradient: r along rows (j,k)=(ta,tb), s along columns (i,k)=(ta,tb), t along (i,j)=(ta,tb)
-  double wt[KH], dvh[KH];
-  {
-    double l[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(m, ta, tb)];
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(o0i + q, m) * l[m];
-      sr[IDX(o0i + q, ta, tb)] = v;
-    }
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, m, tb)];
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(o0i + q, m) * l[m];
-      ss[IDX(ta, o0i + q, tb)] = v;
-    }
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[IDX(ta, tb, m)];
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(o0i + q, m) * l[m];
-      wt[q] = v;  // u_t at (ta, tb, o0i+q)
-      dvh[q] = l[o0i + q];
-    }
-  }
-  __syncthreads();
-  mbar_wait(bar, 0);
-  // geometric factors on the (i,j) column, k in this thread's half
-  {
-    const int i = ta, j = tb;
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      const int k = o0i + q;
-      const int l = (k * N1 + j) * N1 + i;
-      const double ur = sr[IDX(i, j, k)], us = ss[IDX(i, j, k)], ut = wt[q];
-      const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
-      const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
-      sr[IDX(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
-      ss[IDX(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
-      wt[q] = g2 * ur + g4 * us + g5 * ut;
-    }
-  }
-  __syncthreads();
-  // divergence r: rows -> su
-  {
-    double l[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = sr[IDX(m, ta, tb)];
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, o0i + q) * l[m];
-      su[IDX(o0i + q, ta, tb)] = v;
-    }
-  }
-  __syncthreads();
-  // sr is free: publish w_t so every thread can read whole k-columns
-#pragma unroll
-  for (int q = 0; q < KH; ++q) sr[IDX(ta, tb, o0i + q)] = wt[q];
-  // divergence s: columns accumulate into su (disjoint from the sr writes above)
-  {
-    double l[N1];
-#pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = ss[IDX(ta, m, tb)];
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      double v = 0.0;
-#pragma unroll
-      for (int m = 0; m < N1; ++m) v += CD(m, o0i + q) * l[m];
-      su[IDX(ta, o0i + q, tb)] += v;
-    }
-  }
-  __syncthreads();
-  // divergence t + epilogue on the (i,j) column, k in this thread's half
-  const int i = ta, j = tb;
-  const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
-  double l[N1];
-#pragma unroll
-  for (int m = 0; m < N1; ++m) l[m] = sr[IDX(i, j, m)];
-#pragma unroll
-  for (int q = 0; q < KH; ++q) {
-    const int k = o0i + q;
-    double v = 0.0;
-#pragma unroll
-    for (int m = 0; m < N1; ++m) v += CD(m, k) * l[m];
-    v += su[IDX(i, j, k)];
-    if (ij_interior && k >= 1 && k < N) {
-      const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      if constexpr (NOPS > 0) a0 = so[p];
-      if constexpr (NOPS > 1) a1 = so[NIP + p];
-      if constexpr (NOPS > 2) a2 = so[2 * NIP + p];
-      epilogue<EPI>(A, e * NOS + p, v, dvh[q], a0, a1, a2);
-    } else {
-      A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
-    }
-  }
-#undef IDX
-#undef CD
-}
 
 #include "k_sem_k1.cuh"
 
@@ -866,31 +319,6 @@ __global__ void k_sem_k1_lvec(SemArgs A) {
 // Contributor table per shared slot s: up to 8 packed entries
 // (shell index | dx<<16 | dy<<17 | dz<<18) in the fixed (dz, dy, dx) order,
 // so every contribution load is independent (no lut -> shell dependency).
-template <int N>
-struct K2Table {
-  static constexpr int NSH = sem_nshared(N);
-  int cnt[NSH];
-  int ent[NSH][8];
-};
-
-template <int N>
-__device__ __forceinline__ void k2_build_table(K2Table<N>* T, const int* lut) {
-  constexpr int N1 = N + 1, NSH = sem_nshared(N);
-  for (int s = threadIdx.x; s < NSH; s += blockDim.x) {
-    int a, b, c;
-    sem_shared_abc(N, s, a, b, c);
-    const int i = a + 1, j = b + 1, k = c + 1;
-    const int nz = (k == N) ? 2 : 1, ny = (j == N) ? 2 : 1, nx = (i == N) ? 2 : 1;
-    int n = 0;
-    for (int dz = 0; dz < nz; ++dz)
-      for (int dy = 0; dy < ny; ++dy)
-        for (int dx = 0; dx < nx; ++dx) {
-          const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
-          T->ent[s][n++] = lut[(lk * N1 + lj) * N1 + li] | (dx << 16) | (dy << 17) | (dz << 18);
-        }
-    T->cnt[s] = n;
-  }
-}
 
 template <int N, int EPI>
 __global__ void k_sem_k2(SemArgs A) {
@@ -963,21 +391,6 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
     } else {
       k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
     }
-  } else if constexpr (MODE == SEM_AX && N >= 5) {
-    // persistent register-blocked line kernel, double-buffered TMA / cp.async prefetch
-    constexpr std::size_t smem = K4Smem<N, EPI>::bytes;
-    constexpr int nt = (N + 1) * (N + 1);
-    static int grid_cap = 0;
-    if (grid_cap == 0) {
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_v4<N, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0, dev = 0, nsm = 0;
-      CMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sem_k1_v4<N, EPI>, nt, smem));
-      CMG_CUDA(cudaGetDevice(&dev));
-      CMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      grid_cap = std::max(1, per_sm) * nsm;
-    }
-    const long grid = std::min<long>(ne, grid_cap);
-    k_sem_k1_v4<N, EPI><<<(unsigned)grid, nt, smem, s>>>(a);
   } else if constexpr (MODE == SEM_AX) {
     // low orders (coarse p-levels): several elements per block, k-split columns
     constexpr std::size_t smem = K1Smem<N, EPI>::bytes;

@@ -64,6 +64,7 @@ def main():
                "x_sample": [float(v).hex() for v in xc[:: max(1, xc.size // 64)]]}
         with open(args.out, "w") as fh:
             json.dump(res, fh)
+        np.save(args.out + ".x.npy", xc)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
