@@ -385,7 +385,24 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
       if constexpr ((N + 1) % 4 == 0)
         CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    if constexpr ((N + 1) % 4 == 0) {
+    // software-pipelined persistent variant (default) vs one element per block
+    static int pipe_grid = -1;
+    if (pipe_grid < 0) {
+      const char* env = std::getenv("CMG_K1_PIPE");
+      pipe_grid = 0;
+      if (!(env && std::atoi(env) == 0)) {
+        CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_pipe<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0, dev = 0, nsm = 0;
+        CMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sem_k1_pipe<N, EPI, 2>,
+                                                               (N + 1) * (N + 1) * 2, smem));
+        CMG_CUDA(cudaGetDevice(&dev));
+        CMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        pipe_grid = std::max(1, per_sm) * nsm;
+      }
+    }
+    if (pipe_grid > 0 && ks == 2) {
+      k_sem_k1_pipe<N, EPI, 2><<<(unsigned)std::min<long>(ne, pipe_grid), (N + 1) * (N + 1) * 2, smem, s>>>(a);
+    } else if constexpr ((N + 1) % 4 == 0) {
       if (ks == 4) k_sem_k1_lines<N, EPI, 4><<<(unsigned)ne, (N + 1) * (N + 1) * 4, smem, s>>>(a);
       else k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
     } else {
