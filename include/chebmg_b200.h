@@ -126,6 +126,11 @@ int cmg_fd_v_cycle(cmg_fd_hier* h, const cmg_cycle_config* cfg, const double* b,
                    int x_is_zero);                                        /* multigrid.hpp:69-90 */
 int cmg_fd_preconditioner_apply(cmg_fd_hier* h, const cmg_cycle_config* cfg, const double* v,
                                 double* z);                               /* multigrid.hpp:94-98 */
+/* Lanczos approximation constant C (lanczos.hpp:97-155, CEstimate :39-44).
+ * alpha needs room for m doubles, beta for m-1 (either may be NULL);
+ * *steps receives the Lanczos steps taken (alpha.size()). */
+int cmg_fd_estimate_C(cmg_fd_hier* h, size_t m, uint64_t seed, int reorthogonalize, double* C,
+                      double* alpha, double* beta, size_t* steps);
 
 /* ---------------- krylov.hpp ---------------- */
 typedef struct {

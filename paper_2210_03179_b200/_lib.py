@@ -100,6 +100,8 @@ _protos = {
     "cmg_fd_restrict": (C.c_int, [vp, vp, vp]),
     "cmg_fd_coarse_solve": (C.c_int, [vp, vp, vp]),
     "cmg_fd_v_cycle": (C.c_int, [vp, C.POINTER(CycleConfigC), vp, vp, C.c_int]),
+    "cmg_fd_estimate_C": (C.c_int, [vp, sz, C.c_uint64, C.c_int, C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(sz)]),
     "cmg_fd_preconditioner_apply": (C.c_int, [vp, C.POINTER(CycleConfigC), vp, vp]),
     "cmg_precond_fd_vcycle": (C.c_int, [vp, C.POINTER(CycleConfigC), C.POINTER(vp)]),
     "cmg_precond_identity": (C.c_int, [vp, C.POINTER(vp)]),

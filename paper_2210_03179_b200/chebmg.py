@@ -18,7 +18,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass, field
 from enum import IntEnum
-from typing import Callable, Optional
+from typing import Callable, List, Optional
 
 import numpy as np
 import torch
@@ -340,6 +340,31 @@ class Hierarchy:
 def build_hierarchy(dom: Domain, factor: int, eigen_iterations: int = 30, eigen_seed: int = 7,
                     ctx: Optional[Context] = None) -> Hierarchy:
     return Hierarchy(dom, factor, eigen_iterations, eigen_seed, ctx)
+
+
+@dataclass
+class CEstimate:
+    """lanczos.hpp:39-44."""
+
+    C: float = 0.0
+    m: int = 0
+    alpha: List[float] = field(default_factory=list)
+    beta: List[float] = field(default_factory=list)
+
+
+def estimate_C(h: Hierarchy, m: int = 20, seed: int = 99, reorthogonalize: bool = True) -> CEstimate:
+    """Lanczos estimate of the approximation constant C (lanczos.hpp:97-155),
+    run on the device (exact fine solve by fast diagonalisation)."""
+    if m < 1:
+        raise ValueError("estimate_C: need at least one iteration")
+    a = (C.c_double * m)()
+    b = (C.c_double * max(1, m - 1))()
+    cval = C.c_double()
+    steps = C.c_size_t()
+    check(lib.cmg_fd_estimate_C(h.h, m, seed & (2**64 - 1), 1 if reorthogonalize else 0, C.byref(cval), a, b,
+                                C.byref(steps)))
+    k = steps.value
+    return CEstimate(cval.value, m, list(a[:k]), list(b[: max(0, k - 1)]))
 
 
 def v_cycle(h: Hierarchy, cfg: CycleConfig, b: torch.Tensor, x: torch.Tensor, x_is_zero: bool = False) -> None:

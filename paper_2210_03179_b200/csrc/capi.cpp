@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <numbers>
 #include <string>
 #include <vector>
 
@@ -375,6 +376,126 @@ struct VCyclePrecond final : cmg_precond {
     fd_v_cycle(h, cfg, v, z, true);
   }
 };
+
+// Sturm-count bisection for the extreme eigenvalues of the Lanczos tridiagonal
+// (lanczos.hpp:49-83); host arithmetic, m <= a few dozen.
+double tridiag_spectral_radius(const std::vector<double>& a, const std::vector<double>& b) {
+  const std::size_t n = a.size();
+  if (n == 0) fail(CMG_EINVAL, "tridiag_spectral_radius: empty matrix");
+  double lo = a[0], hi = a[0];
+  for (std::size_t i = 0; i < n; ++i) {
+    const double off = (i > 0 ? std::abs(b[i - 1]) : 0.0) + (i + 1 < n ? std::abs(b[i]) : 0.0);
+    lo = std::min(lo, a[i] - off);
+    hi = std::max(hi, a[i] + off);
+  }
+  auto below = [&](double x) {
+    std::size_t cnt = 0;
+    double d = a[0] - x;
+    cnt += d < 0.0;
+    for (std::size_t i = 1; i < n; ++i) {
+      if (d == 0.0) d = 1e-300;
+      d = a[i] - x - b[i - 1] * b[i - 1] / d;
+      cnt += d < 0.0;
+    }
+    return cnt;
+  };
+  const double scale = std::max(std::abs(lo), std::abs(hi)) + 1e-300;
+  auto extreme = [&](bool largest) {
+    double l = lo, u = hi;
+    for (int it = 0; it < 200 && (u - l) > 1e-15 * scale; ++it) {
+      const double mid = 0.5 * (l + u);
+      const std::size_t c = below(mid);
+      const bool keep_upper = largest ? (c == n) : (c == 0);
+      if (keep_upper == largest) u = mid; else l = mid;
+    }
+    return 0.5 * (l + u);
+  };
+  return std::max(std::abs(extreme(true)), std::abs(extreme(false)));
+}
+
+// Lanczos estimate of the approximation constant C (lanczos.hpp:97-155) on the
+// device.  The exact fine solve the reference does with a banded Cholesky of
+// fine_csr (lanczos.hpp:21-37) is a fast-diagonalisation solve here: the
+// 5-point operator is I (x) T/hx^2 + T (x) I/hy^2 with T = tridiag(-1,2,-1),
+// whose eigenvectors are the discrete sines -> 4 mode products per solve.
+void fd_estimate_C(cmg_fd_hier* h, std::size_t m, std::uint64_t seed, bool reorth,
+                   std::vector<double>& alpha, std::vector<double>& beta, double* C) {
+  if (m < 1) fail(CMG_EINVAL, "estimate_C: need at least one iteration");
+  cmg_ctx* c = h->ctx;
+  cudaStream_t s = c->stream;
+  FdOp* A = h->A.get();
+  const int mf = h->mf;
+  const std::size_t n = A->len;
+  // fine sine basis and eigenvalue grid
+  std::vector<double> Sf((std::size_t)mf * mf), lam(mf), Dg(n);
+  const double pi = std::numbers::pi, nrm = std::sqrt(2.0 / (mf + 1));
+  for (int i = 0; i < mf; ++i) {
+    lam[i] = 2.0 - 2.0 * std::cos((i + 1) * pi / (mf + 1));
+    for (int k = 0; k < mf; ++k) Sf[(std::size_t)i * mf + k] = nrm * std::sin((double)(i + 1) * (k + 1) * pi / (mf + 1));
+  }
+  for (int a = 0; a < mf; ++a)
+    for (int b = 0; b < mf; ++b) Dg[(std::size_t)a * mf + b] = lam[b] * A->g.ihx2 + lam[a] * A->g.ihy2;
+  DBuf S(Sf.size()), D(n), t1(n), t2(n), u1(n), u2(n), r(n), Q(m * n), sc(2);
+  CMG_CUDA(cudaMemcpyAsync(S.p, Sf.data(), Sf.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  CMG_CUDA(cudaMemcpyAsync(D.p, Dg.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+  auto fine_solve = [&](const double* rhs, double* out) {
+    mode_product(0, mf, mf, 1, mf, (long)n, S.p, mf, true, rhs, u1.p, nullptr, s);
+    mode_product(1, mf, mf, 1, mf, (long)n, S.p, mf, true, u1.p, u2.p, D.p, s);
+    mode_product(0, mf, mf, 1, mf, (long)n, S.p, mf, false, u2.p, u1.p, nullptr, s);
+    mode_product(1, mf, mf, 1, mf, (long)n, S.p, mf, false, u1.p, out, nullptr, s);
+  };
+  const double lambda_hat = estimate_lambda_max(A, h->invd.p, 200, seed ^ 0x9e3779b97f4a7c15ull);
+  auto project_f = [&](double* u) {  // u -= P A_c^{-1} P^T A u
+    A->apply(u, t1.p);
+    fd_restrict(h->mf, h->mc, (int)h->factor, t1.p, h->rc.p, s);
+    fd_coarse_solve(h, h->rc.p, h->ec.p);
+    fd_prolong(h->mf, h->mc, (int)h->factor, h->ec.p, t2.p, true, s);
+    launch_axpy(n, -1.0, t2.p, u, s);
+  };
+  auto op_inv = [&](const double* q, double* out) {  // lambda_hat * A^{-1} (D q)
+    launch_scal_copy(n, nullptr, A->dval, q, t1.p, s);
+    fine_solve(t1.p, t2.p);
+    launch_scal_copy(n, nullptr, lambda_hat, t2.p, out, s);
+  };
+  double* d0 = sc.p;
+  auto reortho = [&](std::size_t nq) {
+    for (std::size_t i = 0; i < nq; ++i) {
+      launch_dot(Q.p + i * n, r.p, n, c->dpart, d0, s);
+      launch_axpy_dev(n, d0, -1.0, Q.p + i * n, r.p, nullptr, s);
+    }
+  };
+  std::vector<double> q0(n);
+  host_random_vector(n, seed, q0.data());
+  CMG_CUDA(cudaMemcpyAsync(Q.p, q0.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+  project_f(Q.p);
+  launch_norm2(Q.p, n, c->dpart, d0, s);
+  launch_scal_copy(n, d0, 0.0, Q.p, Q.p, s);  // scal(1/||q||, q)
+  alpha.clear();
+  beta.clear();
+  op_inv(Q.p, r.p);
+  project_f(r.p);
+  launch_dot(Q.p, r.p, n, c->dpart, d0, s);
+  alpha.push_back(read_scalar(c, d0));
+  launch_axpy_dev(n, d0, -1.0, Q.p, r.p, nullptr, s);
+  if (reorth) reortho(1);
+  launch_norm2(r.p, n, c->dpart, sc.p + 1, s);
+  double bk = read_scalar(c, sc.p + 1);
+  for (std::size_t k = 2; k <= m && bk != 0.0; ++k) {
+    beta.push_back(bk);
+    double* qk = Q.p + (k - 1) * n;
+    launch_scal_copy(n, sc.p + 1, 0.0, r.p, qk, s);  // q_k = r / beta
+    op_inv(qk, r.p);
+    project_f(r.p);
+    launch_axpy_dev(n, sc.p + 1, -1.0, Q.p + (k - 2) * n, r.p, nullptr, s);
+    launch_dot(qk, r.p, n, c->dpart, d0, s);
+    alpha.push_back(read_scalar(c, d0));
+    launch_axpy_dev(n, d0, -1.0, qk, r.p, nullptr, s);
+    if (reorth) reortho(k);
+    launch_norm2(r.p, n, c->dpart, sc.p + 1, s);
+    bk = read_scalar(c, sc.p + 1);
+  }
+  *C = tridiag_spectral_radius(alpha, beta);
+}
 
 struct IdentityPrecond final : cmg_precond {
   std::size_t len = 0;
@@ -853,6 +974,16 @@ int cmg_fd_restrict(cmg_fd_hier* h, const double* x, double* yc) {
 }
 int cmg_fd_coarse_solve(cmg_fd_hier* h, const double* rc, double* ec) {
   return guard([&] { fd_coarse_solve(h, rc, ec); });
+}
+int cmg_fd_estimate_C(cmg_fd_hier* h, size_t m, uint64_t seed, int reorthogonalize, double* C,
+                      double* alpha, double* beta, size_t* steps) {
+  return guard([&] {
+    std::vector<double> a, b;
+    fd_estimate_C(h, m, seed, reorthogonalize != 0, a, b, C);
+    if (alpha) std::copy(a.begin(), a.end(), alpha);
+    if (beta) std::copy(b.begin(), b.end(), beta);
+    if (steps) *steps = a.size();
+  });
 }
 int cmg_fd_v_cycle(cmg_fd_hier* h, const cmg_cycle_config* cfg, const double* b, double* x,
                    int x_is_zero) {

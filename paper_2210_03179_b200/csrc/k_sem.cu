@@ -385,12 +385,14 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
       if constexpr ((N + 1) % 4 == 0)
         CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    // software-pipelined persistent variant (default) vs one element per block
+    // software-pipelined persistent variant, opt-in (CMG_K1_PIPE=1): measured
+    // 26.0 vs 31.6 GDOF-step/s for one element per block at E=64^3 (128-register
+    // cap spills, 4 blocks/SM; tools/ab_pipe.sh) -- kept as a tuning knob
     static int pipe_grid = -1;
     if (pipe_grid < 0) {
       const char* env = std::getenv("CMG_K1_PIPE");
       pipe_grid = 0;
-      if (!(env && std::atoi(env) == 0)) {
+      if (env && std::atoi(env) == 1) {
         CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_pipe<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0, dev = 0, nsm = 0;
         CMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sem_k1_pipe<N, EPI, 2>,

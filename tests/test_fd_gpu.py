@@ -241,3 +241,25 @@ def test_determinism(cm):
     a = cm.run_case(cfg).report.residual_history
     b = cm.run_case(cfg).report.residual_history
     assert a == b
+
+
+def test_estimate_C_golden(cm, golden):
+    """lanczos.hpp:97-155 on the device vs the reference's C (golden, n=128 Lx=8 f=2 m=20 seed=7).
+    The exact fine solve is a fast-diagonalisation solve instead of the banded
+    Cholesky, so C agrees to rounding of the Lanczos recurrence, not bitwise."""
+    h = cm.build_hierarchy(cm.Domain(8.0, 1.0, 128), 2)
+    est = cm.estimate_C(h, 20, 7)
+    ref = float.fromhex(golden["estimate_C_n128_Lx8_f2_m20_seed7"])
+    assert est.m == 20 and len(est.alpha) == 20 and len(est.beta) == 19
+    assert abs(est.C - ref) <= 1e-9 * ref, (est.C, ref)
+
+
+@pytest.mark.parametrize("n,Lx,f,m,seed", [(32, 1.0, 2, 8, 3), (64, 16.0, 4, 20, 99), (128, 1.0, 8, 12, 5)])
+def test_estimate_C_live_reference(cm, n, Lx, f, m, seed):
+    h = cm.build_hierarchy(cm.Domain(Lx, 1.0, n), f)
+    rh = ob.RefHierarchy(n, Lx, f)
+    ref = ob.ref().ref_estimate_C(rh.h, m, seed)
+    est = cm.estimate_C(h, m, seed)
+    assert abs(est.C - ref) <= 1e-9 * ref, (est.C, ref)
+    with pytest.raises(ValueError):
+        cm.estimate_C(h, 0)
