@@ -320,15 +320,18 @@ __global__ void k_sem_k1_lvec(SemArgs A) {
 // (shell index | dx<<16 | dy<<17 | dz<<18) in the fixed (dz, dy, dx) order,
 // so every contribution load is independent (no lut -> shell dependency).
 
+constexpr int k2_eb(int N) { return sem_nshared(N) >= 256 ? 1 : 256 / sem_nshared(N); }
+
 template <int N, int EPI>
 __global__ void k_sem_k2(SemArgs A) {
+  // block = K2EB consecutive elements of one (ey, ez) row, one thread per owned
+  // shared slot: element coordinates come from the grid, no integer division
   constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N), NSH = sem_nshared(N);
-  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long q = tid / NSH;
-  const int s = (int)(tid - q * NSH);
-  const long e = A.e_begin + q;
-  if (e >= A.e_end) return;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  const int q = threadIdx.x / NSH;
+  const int s = threadIdx.x - q * NSH;
+  const int ex = blockIdx.x * k2_eb(N) + q, ey = blockIdx.y, ez = blockIdx.z;
+  if (q >= k2_eb(N) || ex >= A.Ex) return;
+  const long e = ex + (long)A.Ex * (ey + (long)A.Ey * ez);
   int a, b, c;
   sem_shared_abc(N, s, a, b, c);
   // padding (far domain boundary) is not an unknown
@@ -431,8 +434,9 @@ template <int N, int EPI>
 void launch_k2(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
-  const long threads = ne * sem_nshared(N);
-  k_sem_k2<N, EPI><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a);
+  // e_begin = 0, e_end = Ex*Ey*Ezl (whole local slab)
+  const dim3 grid((unsigned)((a.Ex + k2_eb(N) - 1) / k2_eb(N)), (unsigned)a.Ey, (unsigned)a.Ezl);
+  k_sem_k2<N, EPI><<<grid, k2_eb(N) * sem_nshared(N), 0, s>>>(a);
   CMG_LAUNCH_CHECK();
 }
 
