@@ -114,6 +114,9 @@ typedef struct {
  * separable fast-diagonalisation solve of A_c = P^T A P. */
 int cmg_fd_hierarchy_create(cmg_ctx* ctx, size_t n, double Lx, double Ly, size_t factor,
                             size_t eigen_iterations, uint64_t eigen_seed, cmg_fd_hier** out);
+/* Same hierarchy on another context (stream), lambda_tilde copied instead of
+ * re-estimated: independent scratch for concurrent solves (harness.hpp:186-201). */
+int cmg_fd_hierarchy_clone(const cmg_fd_hier* src, cmg_ctx* ctx, cmg_fd_hier** out);
 int cmg_fd_hierarchy_destroy(cmg_fd_hier* h);
 double cmg_fd_hierarchy_lambda_tilde(const cmg_fd_hier* h);
 cmg_op* cmg_fd_hierarchy_op(cmg_fd_hier* h);

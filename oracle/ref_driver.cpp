@@ -11,13 +11,16 @@
 // reference's smoother and Krylov templates drive it -- the CPU baseline the
 // survey prescribes.
 #include <chebmg/harness.hpp>
+#include <chebmg/io.hpp>
 #include <chebmg/krylov.hpp>
 #include <chebmg/lanczos.hpp>
 #include <chebmg/multigrid.hpp>
 #include <chebmg/problem.hpp>
 #include <chebmg/smoothers.hpp>
 
+#include <algorithm>
 #include <cstring>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 
@@ -354,6 +357,71 @@ int ref_sem_solve(void* pmg, int driver, int family, double lmax_mult, double lm
     std::memcpy(x_out, res.first.data(), n * sizeof(double));
     fill_report(res.second, hist, hist_cap, hist_len, its, mv, converged, status, rho, wall);
   });
+}
+
+// ---- io.hpp text formats (checker for paper_2210_03179_b200/io.py) ----
+
+static std::size_t put(const std::string& s, char* out, std::size_t cap) {
+  if (cap) {
+    const std::size_t n = std::min(s.size(), cap - 1);
+    std::memcpy(out, s.data(), n);
+    out[n] = '\0';
+  }
+  return s.size();
+}
+
+std::size_t ref_format_shortest(double v, char* out, std::size_t cap) {
+  return put(format_shortest(v), out, cap);
+}
+
+// The reference's own sweep (harness.hpp:297-337) on a config text
+// (io.hpp:525-563), emitted as CSV without the wall-time column.
+int ref_sweep_csv(const char* config_text, char* out, std::size_t cap, std::size_t* len) {
+  return guarded([&] {
+    std::istringstream is(config_text);
+    const SweepSpec spec = sweep_spec_from_config(Config::parse(is));
+    const SweepResult sr = sweep(spec);
+    std::ostringstream os;
+    CsvOptions o;
+    o.include_timing = false;
+    write_csv(os, sr.rows, o);
+    *len = put(os.str(), out, cap);
+  });
+}
+
+std::size_t ref_beta_table_csv(char* out, std::size_t cap) {
+  std::ostringstream os;
+  write_beta_table_csv(os);
+  return put(os.str(), out, cap);
+}
+
+// One CSV row (io.hpp:71-84) of a CaseResult assembled from plain fields;
+// C_est / tuned < 0 mean "absent".
+std::size_t ref_csv_row(double Lx, std::size_t factor, int family, std::size_t k, int cycle, int driver,
+                        std::size_t its, std::size_t mv, double rho, double C_est, double lambda_tilde,
+                        double lmin_mult, double tuned, int converged, double wall_sec, int timing,
+                        char* out, std::size_t cap) {
+  CaseResult r;
+  r.cfg.Lx = Lx;
+  r.cfg.factor = factor;
+  r.cfg.family = fam(family);
+  r.cfg.k = k;
+  r.cfg.cycle = cycle == 0 ? Cycle::full : Cycle::one_sided;
+  r.cfg.driver = driver == 0 ? Driver::pcg : driver == 1 ? Driver::pgmres : Driver::mg_solver;
+  r.cfg.lambda_min_multiplier = lmin_mult;
+  r.report.iterations = its;
+  r.report.fine_matvecs = mv;
+  r.report.rho = rho;
+  r.report.converged = converged != 0;
+  r.report.wall_time_sec = wall_sec;
+  r.lambda_tilde = lambda_tilde;
+  if (C_est >= 0) r.C_est = C_est;
+  if (tuned >= 0) r.tuned_lambda_min = tuned;
+  CsvOptions o;
+  o.include_timing = timing != 0;
+  std::ostringstream os;
+  write_csv_row(os, r, o);
+  return put(os.str(), out, cap);
 }
 
 }  // extern "C"

@@ -91,6 +91,7 @@ _protos = {
     "cmg_chebyshev_smooth": (C.c_int, [vp, vp, C.POINTER(ChebConfig), sz, vp, vp, C.c_int]),
     "cmg_beta_coefficients": (C.c_int, [sz, dp]),
     "cmg_fd_hierarchy_create": (C.c_int, [vp, sz, C.c_double, C.c_double, sz, sz, u64, C.POINTER(vp)]),
+    "cmg_fd_hierarchy_clone": (C.c_int, [vp, vp, C.POINTER(vp)]),
     "cmg_fd_hierarchy_destroy": (C.c_int, [vp]),
     "cmg_fd_hierarchy_lambda_tilde": (C.c_double, [vp]),
     "cmg_fd_hierarchy_op": (vp, [vp]),

@@ -70,6 +70,14 @@ class Context:
     def synchronize(self) -> None:
         check(lib.cmg_ctx_synchronize(self.h))
 
+    def __del__(self):
+        if getattr(self, "h", None) and self not in Context._default.values():
+            try:
+                lib.cmg_ctx_destroy(self.h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
     @staticmethod
     def kernel_launches() -> int:
         return int(lib.cmg_ctx_kernel_launches(None))
@@ -247,6 +255,9 @@ class ChebyshevConfig:  # smoothers.hpp:41-57
                                self.lambda_min_multiplier)
 
 
+BETA_MAX_ORDER = 20  # beta_table.hpp:83 (kBetaMaxOrder)
+
+
 def beta_coefficients(k: int) -> list[float]:  # beta_table.hpp:86-92
     out = (C.c_double * max(k, 1))()
     check(lib.cmg_beta_coefficients(k, out))
@@ -309,6 +320,18 @@ class Hierarchy:
         self.lambda_tilde = float(lib.cmg_fd_hierarchy_lambda_tilde(h))
         # Hierarchy::inv_diag (multigrid.hpp:24) -- same values the library holds
         self.inv_diag = jacobi_inverse_diagonal(self.A.diagonal(), self.ctx)
+
+    def _clone_from(self, src: "Hierarchy", ctx: Context) -> None:
+        """Same hierarchy on another context/stream (lambda_tilde copied)."""
+        self.ctx = ctx
+        self.domain = src.domain
+        self.factor = src.factor
+        h = _lib.vp()
+        check(lib.cmg_fd_hierarchy_clone(src.h, ctx.h, C.byref(h)))
+        self.h = h
+        self.A = DeviceOperator(lib.cmg_fd_hierarchy_op(h), ctx, owner=self)
+        self.lambda_tilde = float(lib.cmg_fd_hierarchy_lambda_tilde(h))
+        self.inv_diag = jacobi_inverse_diagonal(self.A.diagonal(), ctx)
 
     def fine_dim(self) -> int:
         return self.A.rows()
@@ -536,6 +559,25 @@ class Driver(IntEnum):
     mg_solver = 2
 
 
+def cycle_from_string(s: str) -> Cycle:  # harness.hpp:28-32
+    try:
+        return Cycle[s]
+    except KeyError:
+        raise ValueError(f"unknown cycle: {s}") from None
+
+
+def driver_from_string(s: str) -> Driver:  # harness.hpp:36-41
+    try:
+        return Driver[s]
+    except KeyError:
+        raise ValueError(f"unknown driver: {s}") from None
+
+
+def _fmt_g(v: float) -> str:
+    """``std::ostream << double`` with the default stream flags (%g, precision 6)."""
+    return f"{v:g}"
+
+
 @dataclass
 class Seeds:  # harness.hpp:52-56
     rhs: int = 1234
@@ -559,12 +601,17 @@ class CaseConfig:  # harness.hpp:62-95
     lambda_max_multiplier: float = 1.03
     lambda_min_multiplier: float = 0.1
     eigen_iterations: int = 30
+    estimate_c: bool = False
 
     def k_pre(self) -> int:
         return self.k if self.cycle == Cycle.full else 2 * self.k
 
     def k_post(self) -> int:
         return self.k if self.cycle == Cycle.full else 0
+
+    def id(self) -> str:  # harness.hpp:82-87
+        return (f"Lx{_fmt_g(self.Lx)}_f{self.factor}_{self.family.name}_k{self.k}_"
+                f"{self.cycle.name}_{self.driver.name}")
 
     def validate(self) -> None:
         if self.k < 1:
@@ -580,6 +627,7 @@ class CaseResult:  # harness.hpp:97-104
     cfg: CaseConfig
     report: SolveReport
     lambda_tilde: float = 0.0
+    C_est: Optional[float] = None
     tuned_lambda_min: Optional[float] = None
     note: str = ""
     x: Optional[torch.Tensor] = None
@@ -595,7 +643,7 @@ def _smoother_config(cfg: CaseConfig, h: Hierarchy, lmin_mult: float) -> Chebysh
 
 
 def dispatch_driver(cfg: CaseConfig, h: Hierarchy, cc: CycleConfig, b: torch.Tensor):
-    """harness.hpp:152-168."""
+    """harness.hpp:152-168 -> (x or None, SolveReport)."""
     M = vcycle_preconditioner(h, cc)
     opts = SolveOptions(tol=cfg.tol, maxit=cfg.maxit, restart=cfg.restart)
     if cfg.driver == Driver.pcg:
@@ -605,23 +653,71 @@ def dispatch_driver(cfg: CaseConfig, h: Hierarchy, cc: CycleConfig, b: torch.Ten
     return None, stationary_solve(h.A, M, b, cfg.tol, cfg.maxit)
 
 
-def tune_lambda_min_empirical(cfg: CaseConfig, h: Hierarchy, candidates: list[float]) -> float:
-    """harness.hpp:188-225: fewest iterations, ties by matvecs, first wins."""
+@dataclass
+class TuneRow:  # harness.hpp:178-181
+    candidate: float
+    report: SolveReport
+
+
+def tune_lambda_min_table(cfg: CaseConfig, h: Hierarchy, candidates: list[float],
+                          concurrent: bool = True) -> list[TuneRow]:
+    """harness.hpp:186-201: one solve per lambda_min candidate against the
+    seeded tuning right-hand side.  The candidate solves are independent, so
+    with ``concurrent`` they run at the same time, each on its own CUDA stream
+    with its own hierarchy scratch (the host threads sit in the library with
+    the GIL released).  Reports are identical to the sequential run: every
+    solve is deterministic and shares no mutable device state."""
     if not candidates:
         raise ValueError("tune_lambda_min_table: no candidates")
-    bt = torch.from_numpy(random_vector(h.fine_dim(), cfg.seeds.tuning)).to(f"cuda:{h.ctx.device}")
-    best = None
-    for cand in candidates:
-        cc = CycleConfig(_smoother_config(cfg, h, cand), cfg.k_pre(), cfg.k_post())
-        _, r = dispatch_driver(cfg, h, cc, bt)
+    dev = f"cuda:{h.ctx.device}"
+    b_tune = torch.from_numpy(random_vector(h.fine_dim(), cfg.seeds.tuning)).to(dev)
+
+    def one(cand: float, hh: Hierarchy) -> TuneRow:
+        cc = CycleConfig(_smoother_config(cfg, hh, cand), cfg.k_pre(), cfg.k_post())
+        return TuneRow(cand, dispatch_driver(cfg, hh, cc, b_tune)[1])
+
+    if not concurrent or len(candidates) == 1:
+        return [one(c, h) for c in candidates]
+    import concurrent.futures as cf
+
+    torch.cuda.synchronize(h.ctx.device)  # b_tune visible to every stream
+
+    def worker(cand: float) -> TuneRow:
+        stream = torch.cuda.Stream(h.ctx.device)
+        with torch.cuda.stream(stream):  # torch-side allocations on the same stream
+            ctx = Context(h.ctx.device, stream)
+            hh = Hierarchy.__new__(Hierarchy)
+            hh._clone_from(h, ctx)
+            row = one(cand, hh)
+            ctx.synchronize()
+        return row
+
+    with cf.ThreadPoolExecutor(max_workers=len(candidates)) as ex:
+        return list(ex.map(worker, candidates))
+
+
+def select_tuned(rows: list[TuneRow]) -> int:
+    """harness.hpp:205-217: fewest iterations, ties by matvecs, first wins;
+    len(rows) when nothing converged."""
+    best = len(rows)
+    for i, row in enumerate(rows):
+        r = row.report
         if not r.converged:
             continue
-        if best is None or r.iterations < best[1].iterations or (
-                r.iterations == best[1].iterations and r.fine_matvecs < best[1].fine_matvecs):
-            best = (cand, r)
-    if best is None:
-        raise RuntimeError("tune_lambda_min_empirical: all candidates failed")
-    return best[0]
+        if best == len(rows) or r.iterations < rows[best].report.iterations or (
+                r.iterations == rows[best].report.iterations and r.fine_matvecs < rows[best].report.fine_matvecs):
+            best = i
+    return best
+
+
+def tune_lambda_min_empirical(cfg: CaseConfig, h: Hierarchy, candidates: list[float],
+                              concurrent: bool = True) -> float:
+    """harness.hpp:219-225."""
+    rows = tune_lambda_min_table(cfg, h, candidates, concurrent)
+    best = select_tuned(rows)
+    if best == len(rows):
+        raise RuntimeError(f"tune_lambda_min_empirical: all candidates failed for case {cfg.id()}")
+    return rows[best].candidate
 
 
 def run_case_with(cfg: CaseConfig, h: Hierarchy) -> CaseResult:
@@ -637,6 +733,8 @@ def run_case_with(cfg: CaseConfig, h: Hierarchy) -> CaseResult:
     prob = build_problem(h.domain, cfg.seeds.rhs, h.ctx)
     cc = CycleConfig(_smoother_config(cfg, h, lmin), cfg.k_pre(), cfg.k_post())
     res.x, res.report = dispatch_driver(cfg, h, cc, prob.b)
+    if cfg.estimate_c:
+        res.C_est = estimate_C(h, 20, cfg.seeds.eigen).C
     return res
 
 
@@ -646,3 +744,91 @@ def run_case(cfg: CaseConfig, ctx: Optional[Context] = None) -> CaseResult:
     dom = Domain(cfg.Lx, 1.0, cfg.n)
     h = build_hierarchy(dom, cfg.factor, cfg.eigen_iterations, cfg.seeds.eigen, ctx)
     return run_case_with(cfg, h)
+
+
+@dataclass
+class SweepSpec:  # harness.hpp:262-269
+    Lx: List[float] = field(default_factory=lambda: [1.0, 8.0, 64.0, 128.0])
+    factors: List[int] = field(default_factory=lambda: [2, 16])
+    families: List[Family] = field(default_factory=lambda: [Family.first, Family.fourth, Family.fourth_opt])
+    ks: List[int] = field(default_factory=lambda: list(range(1, 11)))
+    cycles: List[Cycle] = field(default_factory=lambda: [Cycle.full, Cycle.one_sided])
+    base: CaseConfig = field(default_factory=CaseConfig)
+
+
+@dataclass
+class SweepResult:  # harness.hpp:271-276
+    rows: List[CaseResult] = field(default_factory=list)
+    best_per_group: dict = field(default_factory=dict)
+
+
+def select_best_rows(sr: SweepResult) -> None:
+    """harness.hpp:278-295: per (Lx, factor) the converged row with the fewest
+    fine matvecs, ties by iterations, then smaller k, then row order."""
+    sr.best_per_group = {}
+    for i, r in enumerate(sr.rows):
+        if not r.report.converged:
+            continue
+        key = (r.cfg.Lx, r.cfg.factor)
+        cur = sr.best_per_group.get(key)
+        if cur is None:
+            sr.best_per_group[key] = i
+            continue
+        c = sr.rows[cur]
+        if (r.report.fine_matvecs, r.report.iterations, r.cfg.k) < (c.report.fine_matvecs, c.report.iterations, c.cfg.k):
+            sr.best_per_group[key] = i
+
+
+def sweep_groups(spec: SweepSpec) -> list[tuple[float, int]]:
+    return [(Lx, f) for Lx in spec.Lx for f in spec.factors]
+
+
+def sweep_group_rows(spec: SweepSpec, Lx: float, factor: int, ctx: Optional[Context] = None) -> list[CaseResult]:
+    """The rows of one (Lx, factor) group in reference order (harness.hpp:301-331);
+    a row whose case throws becomes an error row."""
+    import dataclasses
+
+    probe = dataclasses.replace(spec.base, Lx=Lx, factor=factor)
+    probe.validate()
+    h = build_hierarchy(Domain(Lx, 1.0, probe.n), factor, probe.eigen_iterations, probe.seeds.eigen, ctx)
+    C_shared = estimate_C(h, 20, probe.seeds.eigen).C if probe.estimate_c else None
+    rows = []
+    for fam in spec.families:
+        for k in spec.ks:
+            for cyc in spec.cycles:
+                cfg = dataclasses.replace(probe, family=fam, k=k, cycle=cyc, estimate_c=False)
+                try:
+                    r = run_case_with(cfg, h)
+                    r.x = None
+                    r.C_est = C_shared
+                except Exception as e:  # noqa: BLE001 -- the reference catches std::exception
+                    r = CaseResult(cfg, SolveReport(residual_history=[0.0], status=f"error: {e}"), h.lambda_tilde)
+                rows.append(r)
+    return rows
+
+
+def sweep(spec: SweepSpec, ctx: Optional[Context] = None, rank: int = 0, world: int = 1) -> SweepResult:
+    """harness.hpp:297-337.  With world > 1 the (Lx, factor) groups are dealt
+    round-robin to the ranks (one GPU each); every rank returns the rows of its
+    groups and ``merge_sweep`` restores the reference row order."""
+    out = SweepResult()
+    for gi, (Lx, f) in enumerate(sweep_groups(spec)):
+        if gi % world == rank:
+            out.rows.extend(sweep_group_rows(spec, Lx, f, ctx))
+    select_best_rows(out)
+    return out
+
+
+def merge_sweep(spec: SweepSpec, per_rank: list[SweepResult]) -> SweepResult:
+    """Reassemble rank results (from ``sweep(..., rank, world)``) in reference row order."""
+    world = len(per_rank)
+    groups = sweep_groups(spec)
+    queues = [list(p.rows) for p in per_rank]
+    out = SweepResult()
+    per_group = len(spec.families) * len(spec.ks) * len(spec.cycles)
+    for gi, _ in enumerate(groups):
+        q = queues[gi % world]
+        out.rows.extend(q[:per_group])
+        del q[:per_group]
+    select_best_rows(out)
+    return out

@@ -329,6 +329,7 @@ double estimate_lambda_max(cmg_op* A, const double* invd, std::size_t iterations
 struct cmg_fd_hier {
   cmg_ctx* ctx = nullptr;
   std::size_t nfine = 0, factor = 0;
+  double Lx = 1.0, Ly = 1.0;
   int mf = 0, mc = 0;
   std::unique_ptr<FdOp> A;
   DBuf invd;
@@ -921,39 +922,57 @@ int cmg_beta_coefficients(size_t k, double* out) {
   });
 }
 
+namespace {
+std::unique_ptr<cmg_fd_hier> fd_hier_build(cmg_ctx* c, size_t n, double Lx, double Ly, size_t factor) {
+  if (factor < 2 || n % factor != 0)
+    fail(CMG_EINVAL, "build_hierarchy: factor must divide n");  // multigrid.hpp:39-40
+  if (n / factor < 2)
+    fail(CMG_EINVAL, "interp_1d: coarse resolution must divide n and leave interior points");
+  auto h = std::make_unique<cmg_fd_hier>();
+  h->ctx = c;
+  h->nfine = n;
+  h->factor = factor;
+  h->Lx = Lx;
+  h->Ly = Ly;
+  h->A = std::make_unique<FdOp>(c, n, Lx, Ly);
+  h->mf = h->A->g.m;
+  h->mc = static_cast<int>(n / factor - 1);
+  const std::size_t nf = h->A->len, nc = (std::size_t)h->mc * h->mc;
+  cudaStream_t s = c->stream;
+  h->invd.alloc(nf);
+  launch_set(nf, 1.0 / h->A->dval, h->invd.p, s);  // jacobi_inverse_diagonal(A.diagonal())
+  std::vector<double> S, lam;
+  host_fd_coarse_eig((int)n, (int)factor, S, lam);
+  const double hx = Lx / static_cast<double>(n), hy = Ly / static_cast<double>(n);
+  std::vector<double> Dg(nc);
+  for (int a = 0; a < h->mc; ++a)
+    for (int bb = 0; bb < h->mc; ++bb) Dg[(std::size_t)a * h->mc + bb] = lam[bb] / (hx * hx) + lam[a] / (hy * hy);
+  h->S.alloc(nc);
+  h->Dg.alloc(nc);
+  CMG_CUDA(cudaMemcpyAsync(h->S.p, S.data(), nc * sizeof(double), cudaMemcpyHostToDevice, s));
+  CMG_CUDA(cudaMemcpyAsync(h->Dg.p, Dg.data(), nc * sizeof(double), cudaMemcpyHostToDevice, s));
+  h->rc.alloc(nc); h->ec.alloc(nc); h->t1.alloc(nc); h->t2.alloc(nc); h->r.alloc(nf);
+  h->r.zero(s);
+  c->sync();  // host vectors S, Dg go out of scope
+  return h;
+}
+}  // namespace
+
 int cmg_fd_hierarchy_create(cmg_ctx* c, size_t n, double Lx, double Ly, size_t factor,
                             size_t eigen_iterations, uint64_t eigen_seed, cmg_fd_hier** out) {
   return guard([&] {
-    if (factor < 2 || n % factor != 0)
-      fail(CMG_EINVAL, "build_hierarchy: factor must divide n");  // multigrid.hpp:39-40
-    if (n / factor < 2)
-      fail(CMG_EINVAL, "interp_1d: coarse resolution must divide n and leave interior points");
-    auto h = std::make_unique<cmg_fd_hier>();
-    h->ctx = c;
-    h->nfine = n;
-    h->factor = factor;
-    h->A = std::make_unique<FdOp>(c, n, Lx, Ly);
-    h->mf = h->A->g.m;
-    h->mc = static_cast<int>(n / factor - 1);
-    const std::size_t nf = h->A->len, nc = (std::size_t)h->mc * h->mc;
-    cudaStream_t s = c->stream;
-    h->invd.alloc(nf);
-    launch_set(nf, 1.0 / h->A->dval, h->invd.p, s);  // jacobi_inverse_diagonal(A.diagonal())
-    std::vector<double> S, lam;
-    host_fd_coarse_eig((int)n, (int)factor, S, lam);
-    const double hx = Lx / static_cast<double>(n), hy = Ly / static_cast<double>(n);
-    std::vector<double> Dg(nc);
-    for (int a = 0; a < h->mc; ++a)
-      for (int bb = 0; bb < h->mc; ++bb) Dg[(std::size_t)a * h->mc + bb] = lam[bb] / (hx * hx) + lam[a] / (hy * hy);
-    h->S.alloc(nc);
-    h->Dg.alloc(nc);
-    CMG_CUDA(cudaMemcpyAsync(h->S.p, S.data(), nc * sizeof(double), cudaMemcpyHostToDevice, s));
-    CMG_CUDA(cudaMemcpyAsync(h->Dg.p, Dg.data(), nc * sizeof(double), cudaMemcpyHostToDevice, s));
-    h->rc.alloc(nc); h->ec.alloc(nc); h->t1.alloc(nc); h->t2.alloc(nc); h->r.alloc(nf);
-    h->r.zero(s);
+    auto h = fd_hier_build(c, n, Lx, Ly, factor);
     h->lambda_tilde = estimate_lambda_max(h->A.get(), h->invd.p, eigen_iterations, eigen_seed);
     h->A->count = 0;  // multigrid.hpp:46
     c->sync();
+    *out = h.release();
+  });
+}
+
+int cmg_fd_hierarchy_clone(const cmg_fd_hier* src, cmg_ctx* c, cmg_fd_hier** out) {
+  return guard([&] {
+    auto h = fd_hier_build(c, src->nfine, src->Lx, src->Ly, src->factor);
+    h->lambda_tilde = src->lambda_tilde;  // same operator: reuse the estimate
     *out = h.release();
   });
 }

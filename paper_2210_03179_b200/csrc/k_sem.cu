@@ -279,12 +279,13 @@ __constant__ double c_D[8][64];
 // contracted direction: N+1 shared loads, (N+1)^2 DFMAs with constant D,
 // N+1 stores -- one shared access per output instead of 2(N+1).  Rows are
 // padded to N+2 doubles (conflict-free line loads).
-template <int N, int EPI>
+template <int N, int EPI, bool GS = true>
 struct K3Smem {
   static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NPP = N1 * N1 * (N1 + 1);
   static constexpr int NOPS = EpiOps<EPI>::n, NIP = SemC<N>::NINT_PAD;
   static constexpr std::size_t g_off = 0;                                  // [6][NP]  (TMA)
-  static constexpr std::size_t o_off = g_off + (std::size_t)6 * NP;        // [NOPS][NIP] (TMA)
+  static constexpr std::size_t g_len = GS ? (std::size_t)6 * NP : 0;       // 0: factors read to registers
+  static constexpr std::size_t o_off = g_off + g_len;                      // [NOPS][NIP] (TMA)
   static constexpr std::size_t u_off = o_off + (std::size_t)NOPS * NIP;    // [NPP] u, later v
   static constexpr std::size_t r_off = u_off + NPP;                        // [NPP] u_r -> w_r
   static constexpr std::size_t s_off = r_off + NPP;                        // [NPP] u_s -> w_s
@@ -405,7 +406,31 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
         pipe_grid = std::max(1, per_sm) * nsm;
       }
     }
-    if (pipe_grid > 0 && ks == 2) {
+    static int greg = -1;
+    if (greg < 0) {
+      // default: factors to registers -- 36.4 vs 33.8 GDOF-step/s for the
+      // shared-memory-staged factors at E=64^3 (tools/ab_env.sh CMG_K1_GREG)
+      const char* env = std::getenv("CMG_K1_GREG");
+      greg = env ? std::atoi(env) : 1;  // 1: KS=2 / 8 blocks per SM; 2: KS=4; 3, 4: 10 / 6 blocks
+      if ((N + 1) % 4 != 0 && greg == 2) greg = 1;
+      constexpr int gb = (int)K3Smem<N, EPI, false>::bytes;
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
+      if constexpr ((N + 1) % 4 == 0)
+        CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
+    }
+    constexpr std::size_t gsm = K3Smem<N, EPI, false>::bytes;
+    constexpr unsigned nt2 = (N + 1) * (N + 1) * 2;
+    if (greg == 1) {
+      k_sem_k1_greg<N, EPI, 2, 8><<<(unsigned)ne, nt2, gsm, s>>>(a);
+    } else if (greg == 3) {
+      k_sem_k1_greg<N, EPI, 2, 10><<<(unsigned)ne, nt2, gsm, s>>>(a);
+    } else if (greg == 4) {
+      k_sem_k1_greg<N, EPI, 2, 6><<<(unsigned)ne, nt2, gsm, s>>>(a);
+    } else if (greg == 2) {
+      if constexpr ((N + 1) % 4 == 0) k_sem_k1_greg<N, EPI, 4, 4><<<(unsigned)ne, 2 * nt2, gsm, s>>>(a);
+    } else if (pipe_grid > 0 && ks == 2) {
       k_sem_k1_pipe<N, EPI, 2><<<(unsigned)std::min<long>(ne, pipe_grid), (N + 1) * (N + 1) * 2, smem, s>>>(a);
     } else if constexpr ((N + 1) % 4 == 0) {
       if (ks == 4) k_sem_k1_lines<N, EPI, 4><<<(unsigned)ne, (N + 1) * (N + 1) * 4, smem, s>>>(a);

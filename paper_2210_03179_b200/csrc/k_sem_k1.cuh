@@ -133,6 +133,29 @@ struct K1L {
     }
   }
 
+  // same as geometry() with the factors read straight from HBM into registers
+  // (coalesced: consecutive threads own consecutive i of one (j,k) row)
+  template <int H>
+  __device__ static void geometry_reg(const double* __restrict__ Ge, double* sr, double* ss, int i, int j,
+                                      double* wt) {
+    constexpr int O0 = H * KH;
+    double g[6][KH];
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      const int l = ((O0 + q) * N1 + j) * N1 + i;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) g[f][q] = __ldg(Ge + f * NP + l);
+    }
+#pragma unroll
+    for (int q = 0; q < KH; ++q) {
+      const int k = O0 + q;
+      const double ur = sr[idx(i, j, k)], us = ss[idx(i, j, k)], ut = wt[q];
+      sr[idx(i, j, k)] = g[0][q] * ur + g[1][q] * us + g[2][q] * ut;
+      ss[idx(i, j, k)] = g[1][q] * ur + g[3][q] * us + g[4][q] * ut;
+      wt[q] = g[2][q] * ur + g[4][q] * us + g[5][q] * ut;
+    }
+  }
+
   template <int H>
   __device__ static void div_r(const double* sr, double* su, int ta, int tb) {
     constexpr int O0 = H * KH;
@@ -248,6 +271,55 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
   __syncthreads();
   ON_PART(div_s, ss, su, sr, ta, tb, wt);
   __syncthreads();
+  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
+}
+
+// Variant without the 24.6 KB shared-memory stage for the geometric factors:
+// they are read into registers in the geometry phase, so a block needs only
+// the u/r/s line buffers and the epilogue operands (~19 KB at N=7) and twice
+// as many elements are resident per SM to hide the HBM latency.
+template <int N, int EPI, int KS, int MINB>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(SemArgs A) {
+  using L = K1L<N, EPI, KS>;
+  using S = K3Smem<N, EPI, false>;
+  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOPS = S::NOPS, NIP = S::NIP, KH = L::KH;
+  constexpr bool HAS_OPS = NOPS > 0 && sem_nint(N) > 0;
+  extern __shared__ __align__(128) double sm[];
+  double* so = sm + S::o_off;
+  double* su = sm + S::u_off;
+  double* sr = sm + S::r_off;
+  double* ss = sm + S::s_off;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
+  const int t = threadIdx.x;
+  const long e = A.e_begin + blockIdx.x;
+  const int line = t % (N1 * N1);
+  const int h = t / (N1 * N1);
+  const int ta = line % N1, tb = line / N1;
+  if constexpr (HAS_OPS) {
+    if (t == 0) {  // TMA of the interior epilogue operands
+      const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
+      mbar_init(bar, 1);
+      mbar_expect_tx(bar, (NOPS - (skip_x ? 1 : 0)) * NIP * 8);
+#pragma unroll
+      for (int op = 0; op < NOPS; ++op) {
+        if (op == 0 && skip_x) continue;
+        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * sem_nos(N), NIP * 8, bar);
+      }
+    }
+  }
+  const double* Ge = A.G + e * 6 * NP;
+  double wt[KH], dvh[KH];
+  ON_PART(gather, A, su, ta, tb, e);
+  __syncthreads();
+  ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
+  __syncthreads();
+  ON_PART(geometry_reg, Ge, sr, ss, ta, tb, wt);
+  __syncthreads();
+  ON_PART(div_r, sr, su, ta, tb);
+  __syncthreads();
+  ON_PART(div_s, ss, su, sr, ta, tb, wt);
+  __syncthreads();
+  if constexpr (HAS_OPS) mbar_wait(bar, 0);
   ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
 }
 

@@ -263,3 +263,68 @@ def test_estimate_C_live_reference(cm, n, Lx, f, m, seed):
     assert abs(est.C - ref) <= 1e-9 * ref, (est.C, ref)
     with pytest.raises(ValueError):
         cm.estimate_C(h, 0)
+
+
+def test_concurrent_tuning_identical_to_sequential(cm):
+    """harness.hpp:186-201: the 16 lambda_min candidate solves run concurrently
+    (one stream + hierarchy clone each) and give the sequential reports exactly."""
+    cfg = cm.CaseConfig(Lx=1.0, n=64, factor=2, family=cm.Family.first_opt_lambda, k=2, cycle=cm.Cycle.full)
+    h = cm.build_hierarchy(cm.Domain(1.0, 1.0, 64), 2)
+    cands = cm.default_tuning_candidates()
+    seq = cm.tune_lambda_min_table(cfg, h, cands, concurrent=False)
+    par = cm.tune_lambda_min_table(cfg, h, cands, concurrent=True)
+    for a, b in zip(seq, par):
+        assert a.candidate == b.candidate
+        assert (a.report.iterations, a.report.fine_matvecs, a.report.converged) == (
+            b.report.iterations, b.report.fine_matvecs, b.report.converged)
+        assert a.report.residual_history == b.report.residual_history
+    assert cm.select_tuned(seq) == cm.select_tuned(par)
+
+
+def _ref_sweep_rows(cfg_text):
+    import ctypes as C
+    import io as _io
+
+    from paper_2210_03179_b200 import io as cio
+
+    L = ob.ref()
+    L.ref_sweep_csv.restype = C.c_int
+    L.ref_sweep_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    buf = C.create_string_buffer(1 << 20)
+    n = C.c_size_t()
+    assert L.ref_sweep_csv(cfg_text.encode(), buf, len(buf), C.byref(n)) == 0, ob.ref().ref_last_error()
+    return cio.parse_csv(_io.StringIO(buf.value.decode()))
+
+
+def test_sweep_csv_matches_reference_sweep(cm, tmp_path):
+    """The reference's sweep (harness.hpp:297-337) and ours on the same config
+    text: identical rows (ids, counts, convergence, lambda_tilde bits, tuned
+    lambda_min, C) with rho / C within the fp64 tolerance; the best row per
+    group is the same."""
+    import io as _io
+
+    from paper_2210_03179_b200 import io as cio
+
+    text = ("sweep.Lx = 1, 64\nsweep.factor = 2, 4\nsweep.k = 1..3\n"
+            "sweep.family = first, first_opt_lambda, fourth, fourth_opt\nsweep.cycle = full, one_sided\n"
+            "case.n = 32\ncase.driver = pgmres\ncase.tol = 1e-8\ncase.estimate_c = true\n")
+    ref = _ref_sweep_rows(text)
+    spec = cio.sweep_spec_from_config(cio.Config.parse(_io.StringIO(text)))
+    sr = cm.sweep(spec)
+    out = cio.emit_sweep(sr, str(tmp_path), opts=cio.CsvOptions(include_timing=False))
+    with open(out[0]) as fh:
+        mine = cio.parse_csv(fh)
+    assert len(mine) == len(ref) == 2 * 2 * 4 * 3 * 2
+    for a, b in zip(mine, ref):
+        assert (a.case_id, a.Lx, a.factor, a.family, a.k_pre, a.k_post, a.cycle, a.driver) == (
+            b.case_id, b.Lx, b.factor, b.family, b.k_pre, b.k_post, b.cycle, b.driver)
+        assert (a.iterations, a.fine_matvecs, a.converged, a.lambda_tilde, a.lambda_min_mult) == (
+            b.iterations, b.fine_matvecs, b.converged, b.lambda_tilde, b.lambda_min_mult), a.case_id
+        assert abs(a.rho - b.rho) <= 1e-9 * b.rho
+        assert abs(a.C_est - b.C_est) <= 1e-9 * b.C_est
+        assert a.time_ms is None
+    # best row per (Lx, factor): fewest matvecs, then iterations, then k
+    ref_sr = cm.SweepResult([cm.CaseResult(r.cfg, cm.SolveReport(b.iterations, b.fine_matvecs, converged=b.converged))
+                             for r, b in zip(sr.rows, ref)])
+    cm.select_best_rows(ref_sr)
+    assert ref_sr.best_per_group == sr.best_per_group
