@@ -257,8 +257,12 @@ def main():
     step_s = ms_per_step * 1e-3 / order
     peak, peak_src = peaks()
     achieved = per_gpu_bytes / step_s / 1e9
+    # measured DRAM traffic of the same pair: ncu --set full at E=64^3 (profiles/r01/sem_step_E64_summary.txt),
+    # K1 10.664 GB + K2 2.527 GB per step, scaled per element to this run's slab
+    traffic = (10.664e9 + 2.527e9) / 64 ** 3 * (E ** 3 / world)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "fused Chebyshev-Jacobi step (sem K1 element kernel + K2 shared-node kernel)",
+            "traffic": traffic, "traffic_source": "ncu dram__bytes_read+write, K1+K2 per step, profiles/r01",
+            "kernel": "fused Chebyshev-Jacobi step (sem K1 element kernel + K2 shared-node kernel)",
             "algorithmic_bytes_per_step": per_gpu_bytes, "peak_source": peak_src}
 
     # e2e through the public API with host buffers: H2D b,x ; sweep ; D2H x
