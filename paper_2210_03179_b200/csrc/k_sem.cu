@@ -378,66 +378,24 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
   if constexpr (MODE == SEM_AX && N >= 5 && (N + 1) % 2 == 0) {
-    // line-contraction kernel (k_sem_k1.cuh): KS threads per line.  KS=2 measured
-    // 31.8 vs 31.0 GDOF-step/s for KS=4 at E=64^3 (tools/ab_split.sh); 4 kept as a knob
-    constexpr std::size_t smem = K3Smem<N, EPI>::bytes;
-    static int ks = 0;
-    if (ks == 0) {
-      const char* env = std::getenv("CMG_K1_SPLIT");  // tuning knob: 2 or 4
-      ks = ((N + 1) % 4 == 0) ? (env && std::atoi(env) == 4 ? 4 : 2) : 2;
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      if constexpr ((N + 1) % 4 == 0)
-        CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
-    // software-pipelined persistent variant, opt-in (CMG_K1_PIPE=1): measured
-    // 26.0 vs 31.6 GDOF-step/s for one element per block at E=64^3 (128-register
-    // cap spills, 4 blocks/SM; tools/ab_pipe.sh) -- kept as a tuning knob
-    static int pipe_grid = -1;
-    if (pipe_grid < 0) {
-      const char* env = std::getenv("CMG_K1_PIPE");
-      pipe_grid = 0;
-      if (env && std::atoi(env) == 1) {
-        CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_pipe<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0, dev = 0, nsm = 0;
-        CMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sem_k1_pipe<N, EPI, 2>,
-                                                               (N + 1) * (N + 1) * 2, smem));
-        CMG_CUDA(cudaGetDevice(&dev));
-        CMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        pipe_grid = std::max(1, per_sm) * nsm;
-      }
-    }
+    // line-contraction kernels (k_sem_k1.cuh), two threads per line.  Default:
+    // geometric factors read to registers (k_sem_k1_greg) -- 36.4 vs 33.8
+    // GDOF-step/s for the TMA/shared-memory-staged factors (k_sem_k1_lines,
+    // CMG_K1_GREG=0) at E=64^3.  Also measured and dropped: 4 threads per line
+    // (30.4), 6 or 10 blocks/SM register caps (35.1 / 34.8), a persistent
+    // software-pipelined element loop (26.0; spills at its register cap).
     static int greg = -1;
     if (greg < 0) {
-      // default: factors to registers -- 36.4 vs 33.8 GDOF-step/s for the
-      // shared-memory-staged factors at E=64^3 (tools/ab_env.sh CMG_K1_GREG)
       const char* env = std::getenv("CMG_K1_GREG");
-      greg = env ? std::atoi(env) : 1;  // 1: KS=2 / 8 blocks per SM; 2: KS=4; 3, 4: 10 / 6 blocks
-      if ((N + 1) % 4 != 0 && greg == 2) greg = 1;
-      constexpr int gb = (int)K3Smem<N, EPI, false>::bytes;
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
-      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
-      if constexpr ((N + 1) % 4 == 0)
-        CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, gb));
+      greg = (env && std::atoi(env) == 0) ? 0 : 1;
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<N, EPI, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)K3Smem<N, EPI, false>::bytes));
+      CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_lines<N, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)K3Smem<N, EPI>::bytes));
     }
-    constexpr std::size_t gsm = K3Smem<N, EPI, false>::bytes;
-    constexpr unsigned nt2 = (N + 1) * (N + 1) * 2;
-    if (greg == 1) {
-      k_sem_k1_greg<N, EPI, 2, 8><<<(unsigned)ne, nt2, gsm, s>>>(a);
-    } else if (greg == 3) {
-      k_sem_k1_greg<N, EPI, 2, 10><<<(unsigned)ne, nt2, gsm, s>>>(a);
-    } else if (greg == 4) {
-      k_sem_k1_greg<N, EPI, 2, 6><<<(unsigned)ne, nt2, gsm, s>>>(a);
-    } else if (greg == 2) {
-      if constexpr ((N + 1) % 4 == 0) k_sem_k1_greg<N, EPI, 4, 4><<<(unsigned)ne, 2 * nt2, gsm, s>>>(a);
-    } else if (pipe_grid > 0 && ks == 2) {
-      k_sem_k1_pipe<N, EPI, 2><<<(unsigned)std::min<long>(ne, pipe_grid), (N + 1) * (N + 1) * 2, smem, s>>>(a);
-    } else if constexpr ((N + 1) % 4 == 0) {
-      if (ks == 4) k_sem_k1_lines<N, EPI, 4><<<(unsigned)ne, (N + 1) * (N + 1) * 4, smem, s>>>(a);
-      else k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
-    } else {
-      k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
-    }
+    constexpr unsigned nt = (N + 1) * (N + 1) * 2;
+    if (greg) k_sem_k1_greg<N, EPI, 2, 8><<<(unsigned)ne, nt, K3Smem<N, EPI, false>::bytes, s>>>(a);
+    else k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, nt, K3Smem<N, EPI>::bytes, s>>>(a);
   } else if constexpr (MODE == SEM_AX) {
     // low orders (coarse p-levels): several elements per block, k-split columns
     constexpr std::size_t smem = K1Smem<N, EPI>::bytes;

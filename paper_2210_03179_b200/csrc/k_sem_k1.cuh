@@ -53,35 +53,6 @@ struct K1L {
     for (int q = 0; q < KH; ++q) su[idx(ta, tb, O0 + q)] = v[q];
   }
 
-  // split gather for the pipelined kernel: issue the loads early, store later
-  template <int H>
-  __device__ static void gather_load(const SemArgs& A, int ta, int tb, long e, double* v) {
-    constexpr int O0 = H * KH;
-    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-    int oex = 0, oey = 0;
-    const int ax = owner1d<N>(ex, ta, A.Ex, oex);
-    const int ay = owner1d<N>(ey, tb, A.Ey, oey);
-    const bool xy_ok = ax >= 0 && ay >= 0;
-#pragma unroll
-    for (int q = 0; q < KH; ++q) {
-      int oez = 0;
-      const int az = owner1d<N>(A.z0 + ez, O0 + q, A.Ez, oez);
-      const int lz = oez - A.z0;
-      const bool ok = xy_ok && az >= 0;
-      const long own = ((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS +
-                       sem_pos(N, xy_ok ? ax : 0, xy_ok ? ay : 0, az >= 0 ? az : 0);
-      const long halo = ((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay;
-      const double* ptr = (lz < 0) ? A.halo_lo + halo : A.u + own;
-      v[q] = ok ? __ldg(ptr) : 0.0;
-    }
-  }
-  template <int H>
-  __device__ static void gather_store(double* su, int ta, int tb, const double* v) {
-    constexpr int O0 = H * KH;
-#pragma unroll
-    for (int q = 0; q < KH; ++q) su[idx(ta, tb, O0 + q)] = v[q];
-  }
-
   template <int H>
   __device__ static void gradient(const double* su, double* sr, double* ss, int ta, int tb, double* wt,
                                   double* dvh) {
@@ -323,86 +294,4 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
   ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
 }
 
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// Persistent, software-pipelined variant: each block walks elements
-// e = e_begin + blockIdx.x + k*gridDim.x and overlaps the NEXT element's
-// traffic with the current element's compute, with a single set of buffers:
-//   - G(e_next) is streamed by TMA as soon as geometry(e) has consumed G(e),
-//   - the gather loads of e_next are issued before the divergence of e (held
-//     in registers) and stored once finish(e) has released the u buffer,
-//   - the interior operand blocks of e_next are streamed after finish(e).
-template <int N, int EPI, int KS>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * KS, 4) k_sem_k1_pipe(SemArgs A) {
-  using L = K1L<N, EPI, KS>;
-  using S = typename L::S;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP, KH = L::KH;
-  constexpr bool HAS_OPS = NOPS > 0 && sem_nint(N) > 0;
-  extern __shared__ __align__(128) double sm[];
-  double* sG = sm + S::g_off;
-  double* so = sm + S::o_off;
-  double* su = sm + S::u_off;
-  double* sr = sm + S::r_off;
-  double* ss = sm + S::s_off;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
-  const int t = threadIdx.x;
-  const int line = t % (N1 * N1);
-  const int h = t / (N1 * N1);
-  const int ta = line % N1, tb = line / N1;
-  const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
-  const unsigned ops_bytes = HAS_OPS ? (NOPS - (skip_x ? 1 : 0)) * NIP * 8 : 0;
-  auto issue_ops = [&](long el) {
-    if constexpr (HAS_OPS) {
-#pragma unroll
-      for (int op = 0; op < NOPS; ++op) {
-        if (op == 0 && skip_x) continue;
-        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + el * NOS, NIP * 8, bar);
-      }
-    }
-  };
-  long e = A.e_begin + blockIdx.x;
-  if (e >= A.e_end) return;  // uniform per block
-  if (t == 0) {
-    mbar_init(bar, 1);
-    mbar_expect_tx(bar, 6 * NP * sizeof(double) + ops_bytes);
-    bulk_g2s(sG, A.G + e * 6 * NP, 6 * NP * sizeof(double), bar);
-    issue_ops(e);
-  }
-  double vg[KH];
-  ON_PART(gather_load, A, ta, tb, e, vg);
-  ON_PART(gather_store, su, ta, tb, vg);
-  __syncthreads();
-  for (unsigned k = 0;; ++k) {
-    const long en = e + gridDim.x;
-    const bool has_next = en < A.e_end;
-    double wt[KH], dvh[KH];
-    ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
-    __syncthreads();
-    mbar_wait(bar, k & 1);
-    ON_PART(geometry, sG, sr, ss, ta, tb, wt);
-    __syncthreads();
-    if (has_next && t == 0) {  // G buffer free: stream the next element's factors
-      fence_proxy_async();
-      mbar_expect_tx(bar, 6 * NP * sizeof(double) + ops_bytes);
-      bulk_g2s(sG, A.G + en * 6 * NP, 6 * NP * sizeof(double), bar);
-    }
-    if (has_next) ON_PART(gather_load, A, ta, tb, en, vg);  // in flight during the divergence
-    ON_PART(div_r, sr, su, ta, tb);
-    __syncthreads();
-    ON_PART(div_s, ss, su, sr, ta, tb, wt);
-    __syncthreads();
-    ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
-    if (!has_next) break;
-    __syncthreads();  // u and operand buffers released by finish(e)
-    if (t == 0) {
-      fence_proxy_async();
-      issue_ops(en);
-    }
-    ON_PART(gather_store, su, ta, tb, vg);
-    __syncthreads();
-    e = en;
-  }
-}
 #undef ON_PART
