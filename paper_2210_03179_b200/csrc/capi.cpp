@@ -369,12 +369,83 @@ void fd_v_cycle(cmg_fd_hier* h, const cmg_cycle_config& cfg, const double* b, do
     chebyshev_smooth(h->A.get(), h->invd.p, cfg.smoother, cfg.k_post, b, x, false);
 }
 
+// preconditioner_apply: one V-cycle from x = 0 (multigrid.hpp:94-98).  The FD
+// cycle is a fixed chain of small launches (≈11 at the n=256 config, each a few
+// microseconds), so each (v, z) pair it is applied to -- PGMRES walks V_j -> Z_j
+// -- is captured once into a CUDA graph and replayed as one launch.  Replays
+// re-add the captured operator applications and kernel launches so the
+// counters read exactly as for direct launches.  CMG_FD_GRAPHS=0 disables.
 struct VCyclePrecond final : cmg_precond {
-  cmg_fd_hier* h;
-  cmg_cycle_config cfg;
+  cmg_fd_hier* h = nullptr;
+  cmg_cycle_config cfg{};
+  struct Captured {
+    const double* v;
+    double* z;
+    cudaGraphExec_t exec;
+    std::size_t applications;
+    unsigned long long launches;
+  };
+  std::vector<Captured> graphs;
+  cudaStream_t cap = nullptr;
+  int use_graphs = -1;
+
+  ~VCyclePrecond() override {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    if (cap) cudaStreamDestroy(cap);
+  }
+
   void apply(const double* v, double* z) override {
-    // preconditioner_apply: one V-cycle from x = 0 (multigrid.hpp:94-98)
-    fd_v_cycle(h, cfg, v, z, true);
+    if (use_graphs < 0) {
+      const char* env = std::getenv("CMG_FD_GRAPHS");
+      use_graphs = (env && std::atoi(env) == 0) ? 0 : 1;
+    }
+    if (!use_graphs || graphs.size() >= 128) {
+      fd_v_cycle(h, cfg, v, z, true);
+      return;
+    }
+    const Captured* g = nullptr;
+    for (const auto& c : graphs)
+      if (c.v == v && c.z == z) g = &c;
+    if (!g) g = capture(v, z);
+    CMG_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+    h->A->count += g->applications;
+    g_kernel_launches += g->launches;
+  }
+
+  const Captured* capture(const double* v, double* z) {
+    // everything that may throw or allocate happens before the capture
+    if (cfg.k_pre > 0 || cfg.k_post > 0) validate_cheb(cfg.smoother);
+    if (cfg.smoother.family == CMG_FOURTH_OPT && std::max(cfg.k_pre, cfg.k_post) > 0 &&
+        !host_beta_row(std::max(cfg.k_pre, cfg.k_post)))
+      fail(CMG_ERANGE, "beta_coefficients: order outside tabulated range 1..20");
+    h->A->ensure_scratch();
+    if (!cap) CMG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CMG_CUDA(cudaStreamSynchronize(ctx->stream));  // scratch initialisation done
+    const std::size_t a0 = h->A->count;
+    const unsigned long long l0 = g_kernel_launches.load();
+    cudaStream_t user = ctx->stream;
+    ctx->stream = cap;
+    cudaGraph_t graph = nullptr;
+    CMG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    try {
+      fd_v_cycle(h, cfg, v, z, true);
+    } catch (...) {
+      cudaStreamEndCapture(cap, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      ctx->stream = user;
+      throw;
+    }
+    ctx->stream = user;
+    CMG_CUDA(cudaStreamEndCapture(cap, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t err = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CMG_CUDA(err);
+    Captured c{v, z, exec, h->A->count - a0, g_kernel_launches.load() - l0};
+    h->A->count = a0;  // captured, not executed
+    g_kernel_launches -= c.launches;
+    graphs.push_back(c);
+    return &graphs.back();
   }
 };
 

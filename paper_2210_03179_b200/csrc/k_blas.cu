@@ -197,33 +197,53 @@ __global__ void k_normalize_if_pos(std::size_t n, const double* __restrict__ w, 
 }
 
 // krylov.hpp:203-227, one thread, reference operation order
+// One warp, H staged in shared memory; lane l owns columns l and l+32 of every
+// rotation, so each entry sees exactly the reference's operations in the
+// reference's order (krylov.hpp:203-227) -- only the schedule is parallel.
 __global__ void k_gmres_lsq(const double* __restrict__ H, int m, int j, const double* beta,
                             double* Hs, double* g, double* y) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int i = 0; i < (m + 1) * m; ++i) Hs[i] = H[i];
-  for (int i = 0; i <= m; ++i) g[i] = 0.0;
-  g[0] = *beta;
-#define HS(i, jj) Hs[(i) * m + (jj)]
+  __shared__ double sh[64 * 65], sg[65], sy[64];
+  const int lane = threadIdx.x;
+  const int ld = j + 1;  // columns 0..j
+  for (int i = lane; i < (j + 2) * ld; i += 32) sh[i] = H[(i / ld) * m + (i % ld)];
+  for (int i = lane; i <= j + 1; i += 32) sg[i] = 0.0;
+  __syncwarp();
+  if (lane == 0) sg[0] = *beta;
+  __syncwarp();
+#define HS(i, jj) sh[(i) * ld + (jj)]
   for (int c = 0; c <= j; ++c) {
     for (int rr = c + 1; rr <= j + 1; ++rr) {
       const double a11 = HS(c, c), a21 = HS(rr, c);
-      if (a21 == 0.0) continue;
+      __syncwarp();
+      if (a21 == 0.0) continue;  // warp-uniform
       const double den = sqrt(a11 * a11 + a21 * a21);
       const double cs = a11 / den, sn = a21 / den;
-      for (int cc = c; cc <= j; ++cc) {
+      for (int cc = c + lane; cc <= j; cc += 32) {
         const double t1 = HS(c, cc), t2 = HS(rr, cc);
         HS(c, cc) = cs * t1 + sn * t2;
         HS(rr, cc) = -sn * t1 + cs * t2;
       }
-      const double t1 = g[c], t2 = g[rr];
-      g[c] = cs * t1 + sn * t2;
-      g[rr] = -sn * t1 + cs * t2;
+      if (lane == 0) {
+        const double t1 = sg[c], t2 = sg[rr];
+        sg[c] = cs * t1 + sn * t2;
+        sg[rr] = -sn * t1 + cs * t2;
+      }
+      __syncwarp();
     }
   }
-  for (int bi = j; bi >= 0; --bi) {
-    double s = g[bi];
-    for (int cc = bi + 1; cc <= j; ++cc) s -= HS(bi, cc) * y[cc];
-    y[bi] = s / HS(bi, bi);
+  if (lane == 0) {
+    for (int bi = j; bi >= 0; --bi) {
+      double s = sg[bi];
+      for (int cc = bi + 1; cc <= j; ++cc) s -= HS(bi, cc) * sy[cc];
+      sy[bi] = s / HS(bi, bi);
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i <= j; i += 32) y[i] = sy[i];
+  for (int i = lane; i <= m; i += 32) g[i] = i <= j + 1 ? sg[i] : 0.0;
+  for (int i = lane; i < (m + 1) * m; i += 32) {
+    const int r = i / m, cc = i % m;
+    Hs[i] = (r <= j + 1 && cc <= j) ? HS(r, cc) : H[i];
   }
 #undef HS
 }

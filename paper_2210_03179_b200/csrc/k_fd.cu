@@ -201,50 +201,50 @@ __global__ void k_fd_prolong(int mf, int mc, int f, const double* __restrict__ e
 
 // Strided small-GEMM "mode product": contract dimension `dim` of a 3D array.
 // out[o, r] = sum_m Mop(o, m) in[m, r]; Mop = M (row-major, ld) or M^T.
-constexpr int TM = 32, TR = 32, TK = 32;
-__global__ void k_mode_product(int nd, int na, int nb, long sd, long sa, long sb,
-                               const double* __restrict__ M, int ld, int transpose,
-                               const double* __restrict__ in, double* __restrict__ out,
-                               const double* __restrict__ div) {
+// 16x16 output tile per 256-thread block (one output per thread, 64 blocks at
+// the n=256 coarse grid), k in tiles of 64 accumulated in ascending order.
+// Loads and stores walk whichever of (k, r) is unit-stride so both stay
+// coalesced for every contracted dimension.
+constexpr int TM = 16, TR = 16, TK = 64;
+__global__ void __launch_bounds__(256) k_mode_product(int nd, int na, int nb, long sd, long sa, long sb,
+                                                      const double* __restrict__ M, int ld, int transpose,
+                                                      const double* __restrict__ in, double* __restrict__ out,
+                                                      const double* __restrict__ div) {
   __shared__ double Ms[TM][TK + 1];
   __shared__ double Bs[TK][TR + 1];
   const int o0 = blockIdx.y * TM, r0 = blockIdx.x * TR;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 256 threads: ty 0..7
-  double acc[4] = {0, 0, 0, 0};
   const int R = na * nb;
+  const bool kfast = sd == 1;  // contracted dimension is the unit-stride one
+  const int t = threadIdx.x;
+  const int oo = kfast ? t % TM : t / TR, ro = kfast ? t / TM : t % TR;
+  double acc = 0.0;
   for (int k0 = 0; k0 < nd; k0 += TK) {
-    for (int e = threadIdx.x; e < TM * TK; e += blockDim.x) {
-      const int oo = e / TK, kk = e % TK;
-      const int o = o0 + oo, k = k0 + kk;
+    for (int e = t; e < TM * TK; e += 256) {
+      const int mo = transpose ? e % TM : e / TK, mk = transpose ? e / TM : e % TK;
+      const int o = o0 + mo, k = k0 + mk;
       double v = 0.0;
       if (o < nd && k < nd) v = transpose ? M[(long)k * ld + o] : M[(long)o * ld + k];
-      Ms[oo][kk] = v;
+      Ms[mo][mk] = v;
     }
-    for (int e = threadIdx.x; e < TK * TR; e += blockDim.x) {
-      const int kk = e / TR, rr = e % TR;
+    for (int e = t; e < TK * TR; e += 256) {
+      const int kk = kfast ? e % TK : e / TR, rr = kfast ? e / TK : e % TR;
       const int k = k0 + kk, r = r0 + rr;
       double v = 0.0;
-      if (k < nd && r < R) v = in[(long)k * sd + (long)(r % na) * sa + (long)(r / na) * sb];
+      if (k < nd && r < R) {
+        const int ra = r % na, rb = r / na;
+        v = in[(long)k * sd + (long)ra * sa + (long)rb * sb];
+      }
       Bs[kk][rr] = v;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int kk = 0; kk < TK; ++kk) {
-      const double bv = Bs[kk][tx];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] += Ms[ty + 8 * q][kk] * bv;
-    }
+    const int kn = min(TK, nd - k0);
+    for (int kk = 0; kk < kn; ++kk) acc += Ms[oo][kk] * Bs[kk][ro];
     __syncthreads();
   }
-  const int r = r0 + tx;
-  if (r >= R) return;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int o = o0 + ty + 8 * q;
-    if (o >= nd) continue;
-    const long idx = (long)o * sd + (long)(r % na) * sa + (long)(r / na) * sb;
-    out[idx] = div ? acc[q] / div[idx] : acc[q];
-  }
+  const int o = o0 + oo, r = r0 + ro;
+  if (o >= nd || r >= R) return;
+  const long idx = (long)o * sd + (long)(r % na) * sa + (long)(r / na) * sb;
+  out[idx] = div ? acc / div[idx] : acc;
 }
 
 inline dim3 grid2d(int m) { return dim3((m + BX - 1) / BX, (m + BY - 1) / BY); }

@@ -333,24 +333,27 @@ __global__ void k_sem_k2(SemArgs A) {
   const int ex = blockIdx.x * k2_eb(N) + q, ey = blockIdx.y, ez = blockIdx.z;
   if (q >= k2_eb(N) || ex >= A.Ex) return;
   const long e = ex + (long)A.Ex * (ey + (long)A.Ey * ez);
-  int a, b, c;
-  sem_shared_abc(N, s, a, b, c);
+  // host-built table (sem.cpp, L1-resident): [count, a|b<<8|c<<16, (offset, dx|dy<<1|dz<<2) x count],
+  // offset = shell position relative to this element's shell block
+  const int* tab = A.k2tab + s * K2TAB_STRIDE;
+  const int n = __ldg(tab), abc = __ldg(tab + 1);
+  const int a = abc & 0xff, b = (abc >> 8) & 0xff, c = abc >> 16;
   // padding (far domain boundary) is not an unknown
   if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
-  const int* tab = A.k2tab + s * 9;  // host-built (sem.cpp), L1-resident
-  const int n = __ldg(tab);
+  const double* sh = A.shell + e * A.nshell;
+  const bool top = ez + 1 >= A.Ezl;  // the dz=1 contributions come from the halo
   double vals[8];
 #pragma unroll
   for (int cidx = 0; cidx < 8; ++cidx) {
     if (cidx < n) {
-      const int p = __ldg(tab + 1 + cidx);
-      const int li = p & 0xffff, dx = (p >> 16) & 1, dy = (p >> 17) & 1, dz = (p >> 18) & 1;
-      if (ez + dz >= A.Ezl) {
+      const int off = __ldg(tab + 2 + 2 * cidx), f = __ldg(tab + 3 + 2 * cidx);
+      if (top && (f & 4)) {
         // halo: k=0 face of the layer above, indexed by (ex', ey', i', j')
+        const int dx = f & 1, dy = (f >> 1) & 1;
         const int i2 = (a + 1) - dx * N, j2 = (b + 1) - dy * N;
         vals[cidx] = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + i2 + N1 * j2];
       } else {
-        vals[cidx] = A.shell[(e + dx + (long)A.Ex * (dy + (long)A.Ey * dz)) * A.nshell + li];
+        vals[cidx] = sh[off];
       }
     }
   }

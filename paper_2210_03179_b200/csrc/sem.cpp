@@ -120,14 +120,29 @@ struct SemLevel final : cmg_op {
                                  (static_cast<long>(N) * Ez - 1));
     const int N1 = N + 1, NP = N1 * N1 * N1;
     // shell LUT and shared-owned list
+    // Shell layout, grouped by the direction (dx,dy,dz) = (i==0, j==0, k==0) of
+    // the node's owner and, inside a group, in the owner's shared-slot order:
+    // K2's threads (one per owned shared slot) then read each neighbour's
+    // contributions as contiguous runs, and the (0,0,0) group is the element's
+    // own shared slots in slot order.
     std::vector<int> lut_h(NP, -1), sh_h;
     nshell = 0;
-    for (int k = 0; k < N1; ++k)
-      for (int j = 0; j < N1; ++j)
-        for (int i = 0; i < N1; ++i) {
-          const bool interior = i >= 1 && i < N && j >= 1 && j < N && k >= 1 && k < N;
-          if (!interior) lut_h[(k * N1 + j) * N1 + i] = nshell++;
-        }
+    {
+      const int nsh = sem_nshared(N);
+      for (int dz = 0; dz < 2; ++dz)
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dx = 0; dx < 2; ++dx)
+            for (int s2 = 0; s2 < nsh; ++s2) {
+              int a2, b2, c2;
+              sem_shared_abc(N, s2, a2, b2, c2);
+              const int io = a2 + 1, jo = b2 + 1, ko = c2 + 1;  // owner-local indices
+              if (io > N || jo > N || ko > N) continue;         // pad slot
+              if ((dx && io != N) || (dy && jo != N) || (dz && ko != N)) continue;
+              const int i = io - dx * N, j = jo - dy * N, k = ko - dz * N;
+              lut_h[(k * N1 + j) * N1 + i] = nshell++;
+            }
+    }
+    if (nshell != NP - (N - 1) * (N - 1) * (N - 1)) fail(CMG_ERUNTIME, "sem: shell layout size mismatch");
     for (int c2 = 0; c2 < N; ++c2)
       for (int b2 = 0; b2 < N; ++b2)
         for (int a2 = 0; a2 < N; ++a2)
@@ -135,23 +150,32 @@ struct SemLevel final : cmg_op {
     nshared = static_cast<int>(sh_h.size());
     lut.upload(lut_h);
     shared.upload(sh_h);
-    // K2 contributor table: per shared slot s (interior-first order) its <= 8
-    // contributions (shell index | dx<<16 | dy<<17 | dz<<18) in fixed (dz,dy,dx) order
+    // K2 contributor table: per shared slot s (interior-first order) its packed
+    // (a,b,c) and its <= 8 contributions in fixed (dz,dy,dx) order, each as the
+    // shell offset relative to the owner's shell block plus the direction bits
     {
       const int nsh = sem_nshared(N);
-      std::vector<int> tab(static_cast<std::size_t>(nsh) * 9, 0);
+      std::vector<int> tab(static_cast<std::size_t>(nsh) * K2TAB_STRIDE, 0);
       for (int s2 = 0; s2 < nsh; ++s2) {
         int a2, b2, c2;
         sem_shared_abc(N, s2, a2, b2, c2);
+        int* row = tab.data() + static_cast<std::size_t>(s2) * K2TAB_STRIDE;
+        row[1] = a2 | (b2 << 8) | (c2 << 16);
         const int i = a2 + 1, j = b2 + 1, k = c2 + 1;
+        if (i > N || j > N || k > N) continue;  // pad slot: no contributions
         int cnt = 0;
         for (int dz = 0; dz < (k == N ? 2 : 1); ++dz)
           for (int dy = 0; dy < (j == N ? 2 : 1); ++dy)
             for (int dx = 0; dx < (i == N ? 2 : 1); ++dx) {
               const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
-              tab[s2 * 9 + 1 + cnt++] = lut_h[(lk * N1 + lj) * N1 + li] | (dx << 16) | (dy << 17) | (dz << 18);
+              const long off = (dx + static_cast<long>(Ex) * (dy + static_cast<long>(Ey) * dz)) * nshell +
+                               lut_h[(lk * N1 + lj) * N1 + li];
+              if (off > 0x7fffffffL) fail(CMG_EINVAL, "sem: element rows too long for the K2 table");
+              row[2 + 2 * cnt] = static_cast<int>(off);
+              row[3 + 2 * cnt] = dx | (dy << 1) | (dz << 2);
+              ++cnt;
             }
-        tab[s2 * 9] = cnt;
+        row[0] = cnt;
       }
       k2tab.upload(tab);
     }

@@ -32,6 +32,9 @@ enum SemEpi : int {
   EPI_ADD = 6         // y += w
 };
 
+// K2 contributor table row: count, packed (a,b,c), then (shell offset, dx|dy<<1|dz<<2) x 8
+constexpr int K2TAB_STRIDE = 18;
+
 struct SemArgs {
   int N = 7;
   int Ex = 1, Ey = 1, Ezl = 1;  // local element grid (Ezl element layers on this rank)
@@ -59,7 +62,7 @@ struct SemArgs {
   double beta = 1, c1 = 0, c2 = 0, c0 = 0, theta = 1;
   double beta_last = 0;  // > 0: last sweep step, final x += beta_k d' fused, r/d' not stored
   int x_zero = 0;
-  const int* k2tab = nullptr;  // K2 contributor table [nshared][9] (count + 8 packed entries)
+  const int* k2tab = nullptr;  // K2 contributor table [nshared][K2TAB_STRIDE] (sem.cpp)
   // element range [e_begin, e_end) processed by this launch (for overlap splits)
   long e_begin = 0, e_end = 0;
 };

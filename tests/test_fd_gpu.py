@@ -318,8 +318,10 @@ def test_sweep_csv_matches_reference_sweep(cm, tmp_path):
     for a, b in zip(mine, ref):
         assert (a.case_id, a.Lx, a.factor, a.family, a.k_pre, a.k_post, a.cycle, a.driver) == (
             b.case_id, b.Lx, b.factor, b.family, b.k_pre, b.k_post, b.cycle, b.driver)
-        assert (a.iterations, a.fine_matvecs, a.converged, a.lambda_tilde, a.lambda_min_mult) == (
-            b.iterations, b.fine_matvecs, b.converged, b.lambda_tilde, b.lambda_min_mult), a.case_id
+        assert (a.iterations, a.fine_matvecs, a.converged, a.lambda_min_mult) == (
+            b.iterations, b.fine_matvecs, b.converged, b.lambda_min_mult), a.case_id
+        # power-iteration norms are tree-reduced on the device: lambda_tilde to rounding
+        assert abs(a.lambda_tilde - b.lambda_tilde) <= 1e-13 * b.lambda_tilde
         assert abs(a.rho - b.rho) <= 1e-9 * b.rho
         assert abs(a.C_est - b.C_est) <= 1e-9 * b.C_est
         assert a.time_ms is None

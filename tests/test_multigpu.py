@@ -52,3 +52,22 @@ def test_partition_bitwise_identical(tmp_path, geometry):
         diff = np.nonzero(xw != x1)[0]
         print(f"W={w}: {diff.size} entries differ, max |dx| = {np.max(np.abs(xw - x1)) if diff.size else 0}")
         assert diff.size == 0, (w, diff[:10], xw[diff[:10]], x1[diff[:10]])
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_sweep_across_ranks_matches_single_gpu(tmp_path):
+    """harness.hpp:297-337 sweep dealt over 2 ranks (tools/sweep.py): the merged
+    CSV (timing column off) is byte-identical to the 1-GPU sweep."""
+    cfg = tmp_path / "sweep.cfg"
+    cfg.write_text("sweep.Lx = 1, 8, 64\nsweep.factor = 2, 4\nsweep.k = 1..2\n"
+                   "sweep.family = first, fourth_opt\nsweep.cycle = full, one_sided\ncase.n = 32\n")
+    script = os.path.join(ROOT, "tools", "sweep.py")
+    out1, out2 = tmp_path / "w1", tmp_path / "w2"
+    subprocess.run([sys.executable, script, "--config", str(cfg), "--out", str(out1), "--no-timing"],
+                   check=True, timeout=600, cwd=ROOT)
+    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                    "--master-addr", "127.0.0.1", "--master-port", "29611", script, "--config", str(cfg),
+                    "--out", str(out2), "--no-timing"], check=True, timeout=600, cwd=ROOT)
+    a = (out1 / "sweep.csv").read_text()
+    b = (out2 / "sweep.csv").read_text()
+    assert a == b and a.count("\n") == 1 + 3 * 2 * 2 * 2 * 2

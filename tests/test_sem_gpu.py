@@ -193,3 +193,30 @@ def test_determinism(cm, sem):
 
 def test_smoke_check(sem):
     assert "SEM" in sem.smoke_check()
+
+
+@pytest.fixture(scope="module")
+def config1_pair(sem):
+    """BASELINE configs[1] at full size: N=7, E=16^3 (1.37M unknowns), p-MG(7,3,1)."""
+    if not ob.ref_available():
+        pytest.skip("oracle/_ref not built")
+    o = ob.OraclePmg((7, 3, 1), 16, 16, 16, lib=ob.ref())
+    P = sem.PMGHierarchy(sem.SemDesc(7, 16, 16, 16), (7, 3, 1))
+    return o, P
+
+
+@pytest.mark.parametrize("fam,kpre,kpost", [(2, 8, 0), (2, 4, 4), (3, 8, 0), (0, 4, 4)])
+def test_config1_full_size_vs_reference(cm, config1_pair, fam, kpre, kpost):
+    """configs[1] (E=16^3) half (2k,0) vs full (k,k) cycles, 1st/4th/opt-4th kind:
+    PGMRES(30) to 1e-8, GPU vs the reference's pgmres template on the restated
+    operator -- same iteration counts, histories and solutions within 1e-10."""
+    o, P = config1_pair
+    assert abs(P.lambda_tilde[0] - o.lambda_tilde[0]) <= 1e-11 * o.lambda_tilde[0]
+    b = o.sem(0).rhs()
+    oref = ob.ref_sem_solve(o, 1, fam, kpre, kpost, b, tol=1e-8)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
+    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
+    assert (rep.iterations, rep.fine_matvecs, rep.converged) == (oref.iterations, oref.fine_matvecs, True)
+    h, hr = np.array(rep.residual_history), np.array(oref.history)
+    assert np.max(np.abs(h - hr)) <= TOL * hr[0]
+    assert np.linalg.norm(P.A.to_canonical(x) - oref.x) <= TOL * np.linalg.norm(oref.x)
