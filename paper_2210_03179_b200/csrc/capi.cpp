@@ -669,9 +669,13 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
       double* Zj = Z.p + (std::size_t)j * L;
       M->apply(Vj, Zj);
       A->apply(Zj, w.p);
-      const int passes = o.reorthogonalize ? 2 : 1;
-      for (int pass = 0; pass < passes; ++pass) {
-        A->mdot(V.p, L, j + 1, w.p, dsc + S_COEF);
+      // CGS(2) (krylov.hpp:186-195): project, subtract, [project again, subtract];
+      // the first subtraction and the second projection share one pass over V
+      A->mdot(V.p, L, j + 1, w.p, dsc + S_COEF);
+      if (o.reorthogonalize) {
+        A->cgs_mdot(V.p, L, j + 1, dsc + S_COEF, w.p, dsc + S_COEF2, H + j, m);
+        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF2, w.p, L, H + j, m, s);
+      } else {
         launch_cgs_update(V.p, L, j + 1, dsc + S_COEF, w.p, L, H + j, m, s);
       }
       double* hj1 = H + (std::size_t)(j + 1) * m + j;

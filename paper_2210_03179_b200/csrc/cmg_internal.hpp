@@ -88,6 +88,11 @@ void launch_lincomb(std::size_t n, double c1, const double* d, double c2, const 
 // CGS: w -= sum_l coef[l] V_l ; h[l*hstride] += coef[l]
 void launch_cgs_update(const double* V, std::size_t ldv, int nv, const double* coef, double* w,
                        std::size_t n, double* hcol, int hstride, cudaStream_t s);
+// fused CGS pass (nv <= kCgsFuseMax): w -= V coef_in, h += coef_in, out = V^T w_new;
+// bit-identical to launch_cgs_update followed by launch_mdot
+constexpr int kCgsFuseMax = 32;
+void launch_cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coef_in, double* w, std::size_t n,
+                     double* hcol, int hstride, double* partials, double* out, cudaStream_t s);
 // V_{j+1} = w / h  if h > 0  (krylov.hpp:197-200)
 void launch_normalize_if_pos(std::size_t n, const double* w, const double* h, double* v,
                              cudaStream_t s);

@@ -39,6 +39,10 @@ struct DBuf {
 struct Comm {
   void* nccl = nullptr;  // ncclComm_t
   int rank = 0, nranks = 1;
+  // side stream for face exchanges that overlap element kernels, and the
+  // events that order it against the compute stream (created with the comm)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr, ev_contrib = nullptr;
   ~Comm();
   // in-place sum over ranks of `count` doubles (device)
   void allreduce_sum(double* buf, std::size_t count, cudaStream_t s);
@@ -57,6 +61,7 @@ struct Comm {
 enum : int {
   S_R0 = 0, S_BETA, S_RT, S_TMP0, S_TMP1, S_RZ, S_RZNEW, S_PAP, S_ALPHA, S_PBETA,
   S_COEF = 64,          // restart+1 CGS coefficients
+  S_COEF2 = 128,        // second CGS pass (restart+1 <= 64)
   S_H = 256,            // (m+1)*m Hessenberg
   S_HS = S_H + 4160,    // copy
   S_G = S_HS + 4160,    // m+1
@@ -146,6 +151,18 @@ struct cmg_op {
   }
   virtual void mdot(const double* V, std::size_t ldv, int nv, const double* w, double* out_dev) {
     cmg::launch_mdot(V, ldv, nv, w, len, ctx->dpart, out_dev, ctx->stream);
+  }
+  // one CGS pass followed by the next pass's projections (krylov.hpp:186-195):
+  // w -= V coef_in ; hcol += coef_in ; out = V^T w.  Same results as the
+  // update and mdot issued separately; fused when nv <= kCgsFuseMax.
+  virtual void cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coef_in, double* w,
+                        double* out_dev, double* hcol, int hstride) {
+    if (nv <= cmg::kCgsFuseMax) {
+      cmg::launch_cgs_mdot(V, ldv, nv, coef_in, w, len, hcol, hstride, ctx->dpart, out_dev, ctx->stream);
+    } else {
+      cmg::launch_cgs_update(V, ldv, nv, coef_in, w, len, hcol, hstride, ctx->stream);
+      mdot(V, ldv, nv, w, out_dev);
+    }
   }
   // set *flag if any unknown's entry of v is exactly zero (storage padding excluded)
   virtual void flag_zero_entries(const double* v, int* flag) {

@@ -65,6 +65,9 @@ namespace cmg {
 
 Comm::~Comm() {
   if (nccl) nccl_api().CommDestroy(static_cast<ncclComm_t>(nccl));
+  for (cudaEvent_t e : {ev_ready, ev_halo, ev_contrib})
+    if (e) cudaEventDestroy(e);
+  if (side) cudaStreamDestroy(side);
 }
 
 void Comm::allreduce_sum(double* buf, std::size_t count, cudaStream_t s) {
@@ -137,6 +140,9 @@ int cmg_ctx_attach_nccl(cmg_ctx* ctx, const unsigned char id_bytes[128], int ran
       ncclComm_t c;
       CMG_NCCL(nccl_api().CommInitRank(&c, nranks, id, rank));
       comm->nccl = c;
+      CMG_CUDA(cudaStreamCreateWithFlags(&comm->side, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&comm->ev_ready, &comm->ev_halo, &comm->ev_contrib})
+        CMG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     ctx->rank = rank;
     ctx->nranks = nranks;

@@ -317,22 +317,19 @@ __global__ void k_sem_k1_lvec(SemArgs A) {
 }
 
 // ---------------------------------------------------------------- K2
-// Contributor table per shared slot s: up to 8 packed entries
-// (shell index | dx<<16 | dy<<17 | dz<<18) in the fixed (dz, dy, dx) order,
-// so every contribution load is independent (no lut -> shell dependency).
+// Contributor table per shared slot s (sem.cpp): the packed (a,b,c) and up to 8
+// (shell offset, direction) entries in the fixed (dz, dy, dx) order, so every
+// contribution load is independent (no lut -> shell dependency).
 
 constexpr int k2_eb(int N) { return sem_nshared(N) >= 256 ? 1 : 256 / sem_nshared(N); }
 
-template <int N, int EPI>
-__global__ void k_sem_k2(SemArgs A) {
-  // block = K2EB consecutive elements of one (ey, ez) row, one thread per owned
-  // shared slot: element coordinates come from the grid, no integer division
-  constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N), NSH = sem_nshared(N);
-  const int q = threadIdx.x / NSH;
-  const int s = threadIdx.x - q * NSH;
-  const int ex = blockIdx.x * k2_eb(N) + q, ey = blockIdx.y, ez = blockIdx.z;
-  if (q >= k2_eb(N) || ex >= A.Ex) return;
-  const long e = ex + (long)A.Ex * (ey + (long)A.Ey * ez);
+// One owned shared node: sum its <= 8 shell contributions in the fixed
+// (dz, dy, dx) order, then the step's epilogue.  CG: read the shell through L2
+// only (the fused step reads contributions its neighbours wrote in the same
+// launch).  Returns without work for padding slots.
+template <int N, int EPI, bool CG>
+__device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey, int ez, int s) {
+  constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N);
   // host-built table (sem.cpp, L1-resident): [count, a|b<<8|c<<16, (offset, dx|dy<<1|dz<<2) x count],
   // offset = shell position relative to this element's shell block
   const int* tab = A.k2tab + s * K2TAB_STRIDE;
@@ -353,7 +350,7 @@ __global__ void k_sem_k2(SemArgs A) {
         const int i2 = (a + 1) - dx * N, j2 = (b + 1) - dy * N;
         vals[cidx] = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + i2 + N1 * j2];
       } else {
-        vals[cidx] = sh[off];
+        vals[cidx] = CG ? __ldcg(sh + off) : sh[off];
       }
     }
   }
@@ -373,6 +370,19 @@ __global__ void k_sem_k2(SemArgs A) {
     if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
   }
   epilogue<EPI>(A, slot, sum, dv, o0, o1, o2);
+}
+
+template <int N, int EPI>
+__global__ void k_sem_k2(SemArgs A) {
+  // block = K2EB consecutive elements of one (ey, ez) row, one thread per owned
+  // shared slot: element coordinates come from the grid, no integer division
+  constexpr int NSH = sem_nshared(N);
+  const int q = threadIdx.x / NSH;
+  const int s = threadIdx.x - q * NSH;
+  const int ex = blockIdx.x * k2_eb(N) + q, ey = blockIdx.y, ez = blockIdx.z + A.k2_z0;
+  if (q >= k2_eb(N) || ex >= A.Ex) return;
+  const long e = ex + (long)A.Ex * (ey + (long)A.Ey * ez);
+  k2_node<N, EPI, false>(A, e, ex, ey, ez, s);
 }
 
 template <int N, int MODE, int EPI>
@@ -420,10 +430,156 @@ template <int N, int EPI>
 void launch_k2(const SemArgs& a, cudaStream_t s) {
   const long ne = a.e_end - a.e_begin;
   if (ne <= 0) return;
-  // e_begin = 0, e_end = Ex*Ey*Ezl (whole local slab)
-  const dim3 grid((unsigned)((a.Ex + k2_eb(N) - 1) / k2_eb(N)), (unsigned)a.Ey, (unsigned)a.Ezl);
-  k_sem_k2<N, EPI><<<grid, k2_eb(N) * sem_nshared(N), 0, s>>>(a);
+  const long per_layer = (long)a.Ex * a.Ey;  // [e_begin, e_end) is whole layers
+  SemArgs b = a;
+  b.k2_z0 = (int)(a.e_begin / per_layer);
+  const dim3 grid((unsigned)((a.Ex + k2_eb(N) - 1) / k2_eb(N)), (unsigned)a.Ey, (unsigned)(ne / per_layer));
+  k_sem_k2<N, EPI><<<grid, k2_eb(N) * sem_nshared(N), 0, s>>>(b);
   CMG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- fused step (K1 + K2 in one launch)
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One element per block, claimed in DECREASING index order through an atomic
+// ticket.  After the element kernel (the k_sem_k1_greg phases) the block
+// publishes "my shell contributions are written" (per-element flag = epoch)
+// and then finishes its own shared nodes itself: their other contributors are
+// its +x/+y/+z neighbours, which have larger indices, hence earlier tickets --
+// they are resident or finished, so the wait cannot deadlock -- and their
+// contributions come back from L2 moments after being written.  The separate
+// K2 launch, the HBM round trip of the shell buffer and one kernel boundary
+// per step disappear; the sums keep K2's fixed (dz, dy, dx) order, so results
+// are bitwise those of the two-kernel path.
+template <int N, int EPI, int KS, int MINB>
+__global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_step_fused(SemArgs A) {
+  using L = K1L<N, EPI, KS>;
+  using S = K3Smem<N, EPI, false>;
+  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOPS = S::NOPS, NIP = S::NIP, KH = L::KH;
+  constexpr int NSH = sem_nshared(N);
+  constexpr bool HAS_OPS = NOPS > 0 && sem_nint(N) > 0;
+  static_assert(NSH <= N1 * N1 * KS, "one thread per owned shared node");
+  extern __shared__ __align__(128) double sm[];
+  __shared__ long e_claim;
+  double* so = sm + S::o_off;
+  double* su = sm + S::u_off;
+  double* sr = sm + S::r_off;
+  double* ss = sm + S::s_off;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
+  const int t = threadIdx.x;
+  if (t == 0)
+    e_claim = A.e_end - 1 -
+              (A.fuse_mode == 0 ? (long)(atomicAdd(A.ticket, 1ull) - A.ticket_base) : (long)blockIdx.x);
+  __syncthreads();
+  const long e = e_claim;
+  const int line = t % (N1 * N1);
+  const int h = t / (N1 * N1);
+  const int ta = line % N1, tb = line / N1;
+  if constexpr (HAS_OPS) {
+    if (t == 0) {
+      const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
+      mbar_init(bar, 1);
+      mbar_expect_tx(bar, (NOPS - (skip_x ? 1 : 0)) * NIP * 8);
+#pragma unroll
+      for (int op = 0; op < NOPS; ++op) {
+        if (op == 0 && skip_x) continue;
+        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * sem_nos(N), NIP * 8, bar);
+      }
+    }
+  }
+  const double* Ge = A.G + e * 6 * NP;
+  double wt[KH], dvh[KH];
+#define ON_PART(fn, ...)                                   \
+  do {                                                     \
+    switch (h) {                                           \
+      case 0: L::template fn<0>(__VA_ARGS__); break;       \
+      case 1: L::template fn<1 % KS>(__VA_ARGS__); break;  \
+      case 2: L::template fn<2 % KS>(__VA_ARGS__); break;  \
+      default: L::template fn<3 % KS>(__VA_ARGS__); break; \
+    }                                                      \
+  } while (0)
+  ON_PART(gather, A, su, ta, tb, e);
+  __syncthreads();
+  ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
+  __syncthreads();
+  ON_PART(geometry_reg, Ge, sr, ss, ta, tb, wt);
+  __syncthreads();
+  ON_PART(div_r, sr, su, ta, tb);
+  __syncthreads();
+  ON_PART(div_s, ss, su, sr, ta, tb, wt);
+  __syncthreads();
+  if constexpr (HAS_OPS) mbar_wait(bar, 0);
+  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
+#undef ON_PART
+  if (A.fuse_mode <= 1) __threadfence();  // this thread's shell stores, device-visible
+  __syncthreads();
+  if (t == 0) {
+    if (A.fuse_mode >= 2) __threadfence();  // block's stores ordered by the barrier (cumulative)
+    st_release_u32(A.flags + e, A.epoch);
+  }
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  if (A.defer_top && ez == A.Ezl - 1) return;  // uniform: K2 after the halo exchange
+  if (A.fuse_mode == 3) return;                 // timing probe only (no shared-node work)
+  if (A.fuse_mode == 5) {
+    // probe: shared-node work without waiting (wrong results)
+  } else if (A.fuse_mode <= 1 || A.fuse_mode == 4) {
+    if (t >= 1 && t < 8) {
+      const int dx = t & 1, dy = (t >> 1) & 1, dz = t >> 2;
+      if (ex + dx < A.Ex && ey + dy < A.Ey && ez + dz < A.Ezl) {
+        const unsigned* f = A.flags + e + dx + (long)A.Ex * (dy + (long)A.Ey * dz);
+        while (ld_acquire_u32(f) != A.epoch) __nanosleep(32);
+      }
+    }
+  } else if (t == 0) {
+    for (int q = 1; q < 8; ++q) {
+      const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+      if (ex + dx < A.Ex && ey + dy < A.Ey && ez + dz < A.Ezl) {
+        const unsigned* f = A.flags + e + dx + (long)A.Ex * (dy + (long)A.Ey * dz);
+        while (ld_acquire_u32(f) != A.epoch) __nanosleep(200);
+      }
+    }
+  }
+  __syncthreads();
+  if (A.fuse_mode == 4) return;  // probe: wait only (wrong results)
+  if (t < NSH) k2_node<N, EPI, true>(A, e, ex, ey, ez, t);
+}
+
+template <int N, int EPI>
+void launch_fused(const SemArgs& a, cudaStream_t s) {
+  const long ne = a.e_end - a.e_begin;
+  if (ne <= 0) return;
+  constexpr std::size_t smem = K3Smem<N, EPI, false>::bytes;
+  static bool configured = false;
+  if (!configured) {
+    CMG_CUDA(cudaFuncSetAttribute(k_sem_step_fused<N, EPI, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    configured = true;
+  }
+  k_sem_step_fused<N, EPI, 2, 8><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
+  CMG_LAUNCH_CHECK();
+}
+
+template <int N>
+bool dispatch_fused(const SemArgs& a, int epi, cudaStream_t s) {
+  if constexpr (N >= 5 && (N + 1) % 2 == 0) {
+    switch (epi) {
+      case EPI_STORE: launch_fused<N, EPI_STORE>(a, s); return true;
+      case EPI_ADD: launch_fused<N, EPI_ADD>(a, s); return true;
+      case EPI_RESID: launch_fused<N, EPI_RESID>(a, s); return true;
+      case EPI_CHEB4: launch_fused<N, EPI_CHEB4>(a, s); return true;
+      case EPI_CHEB1: launch_fused<N, EPI_CHEB1>(a, s); return true;
+      case EPI_CHEB4_INIT: launch_fused<N, EPI_CHEB4_INIT>(a, s); return true;
+      case EPI_CHEB1_INIT: launch_fused<N, EPI_CHEB1_INIT>(a, s); return true;
+    }
+  }
+  return false;
 }
 
 template <int N, int MODE>
@@ -798,6 +954,54 @@ __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int 
   }
 }
 
+// Fused CGS pass over the layered layout: w -= V coef (k_cgs_update's
+// arithmetic) and the per-layer partials of V^T w_new with k_layer_dots' exact
+// chunking and reduction order -- coefficients are bit-identical to the
+// unfused update + layer dots, V is streamed from HBM once.
+__global__ void __launch_bounds__(256) k_layer_cgs_dots(const double* __restrict__ V, std::size_t ldv, int nv,
+                                                        const double* __restrict__ coef, double* __restrict__ w,
+                                                        long layer_len, int nlayers, double* hcol, int hstride,
+                                                        double* __restrict__ partials) {
+  constexpr int MAXV = 32;
+  const int layer = blockIdx.y, chunk = blockIdx.x;
+  __shared__ double c[MAXV];
+  __shared__ double sh[MAXV][8];
+  for (int l = threadIdx.x; l < nv; l += blockDim.x) c[l] = coef[l];
+  __syncthreads();
+  if (layer == 0 && chunk == 0 && threadIdx.x == 0)
+    for (int l = 0; l < nv; ++l) hcol[(std::size_t)l * hstride] += c[l];
+  double acc[MAXV];
+#pragma unroll
+  for (int q = 0; q < MAXV; ++q) acc[q] = 0.0;
+  const long base = (long)layer * layer_len;
+  for (long q = (long)chunk * blockDim.x + threadIdx.x; q < layer_len; q += (long)LCH * blockDim.x) {
+    const std::size_t i = base + q;
+    double v = w[i];
+    // unfused multiply-add, as k_cgs_update (k_blas.cu is built with --fmad=false)
+    for (int l = 0; l < nv; ++l) v = __dadd_rn(v, __dmul_rn(-c[l], V[(std::size_t)l * ldv + i]));
+    w[i] = v;
+#pragma unroll
+    for (int l = 0; l < MAXV; ++l)
+      if (l < nv) acc[l] += V[(std::size_t)l * ldv + i] * v;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int l = 0; l < MAXV; ++l) {
+    if (l < nv) {
+      double v = acc[l];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if (lane == 0) sh[l][warp] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = 0.0;
+    for (int wv = 0; wv < (int)(blockDim.x >> 5); ++wv) s += sh[threadIdx.x][wv];
+    partials[((long)threadIdx.x * nlayers + layer) * LCH + chunk] = s;
+  }
+}
+
 __global__ void k_layer_reduce(const double* __restrict__ partials, int nv, int nlayers,
                                double* __restrict__ out) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -831,6 +1035,13 @@ void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
   CMG_ORDERS(X)
 #undef X
   throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
+}
+
+bool sem_step_fused(const SemArgs& a, int epi, cudaStream_t s) {
+#define X(n) if (a.N == n) return dispatch_fused<n>(a, epi, s);
+  CMG_ORDERS(X)
+#undef X
+  return false;
 }
 
 void sem_k2(const SemArgs& a, int epi, cudaStream_t s) {
@@ -934,6 +1145,16 @@ void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, l
                     int nlayers, double* partials, double* out, cudaStream_t s) {
   dim3 grid(LCH, nlayers, (nv + 7) / 8);
   k_layer_dots<<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+  CMG_LAUNCH_CHECK();
+  const long t = (long)nv * nlayers;
+  k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
+  CMG_LAUNCH_CHECK();
+}
+
+void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* coef, double* w, long layer_len,
+                        int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s) {
+  dim3 grid(LCH, nlayers, 1);
+  k_layer_cgs_dots<<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   CMG_LAUNCH_CHECK();
   const long t = (long)nv * nlayers;
   k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);

@@ -11,6 +11,7 @@
 // Pmg is the p-multigrid hierarchy with the reference's
 // V-cycle control flow (multigrid.hpp:69-90) applied recursively.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -96,6 +97,9 @@ struct SemLevel final : cmg_op {
   int nshell = 0, nshared = 0;
   DBuf G, Dm, xi, w, shell, halo_lo, halo_send, contrib_hi, contrib_send, diagv, mask, Lrhs;
   DBuf lpart, lout, lgath;
+  DBuf fuse_flags, fuse_ticket;  // fused step: per-element epoch flags, element ticket
+  unsigned fuse_epoch = 0;
+  unsigned long long fuse_ticket_total = 0;
   IBuf lut, shared, lpr, k2tab;
   std::vector<int> lpr_h;
 
@@ -278,10 +282,91 @@ struct SemLevel final : cmg_op {
   }
 
   void run(int mode, int epi, SemArgs& a) {
-    if (mode == SEM_AX) exchange_halo(a.u);
-    sem_k1(a, mode, epi, ctx->stream);
-    exchange_contrib();
-    sem_k2(a, epi, ctx->stream);
+    // split-launch overlap of the face exchanges (below), opt-in: measured 67.5
+    // vs 68.3 GDOF-step/s without it at 2 GPUs -- the extra launch tails of the
+    // one-layer K1/K2 pieces cost more than the hidden NCCL latency
+    static const bool overlap = [] {
+      const char* env = std::getenv("CMG_SEM_OVERLAP");
+      return env && std::atoi(env) == 1;
+    }();
+    static const bool fused = [] {  // experimental single-launch step, opt-in
+      const char* env = std::getenv("CMG_SEM_FUSED");
+      return env && std::atoi(env) == 1;
+    }();
+    if (mode == SEM_AX && fused && (N == 5 || N == 7)) {
+      // one launch per operator application (k_sem_step_fused); partitioned:
+      // input halo first, bottom-face contributions down after, then the top
+      // layer's shared nodes (the only ones needing them) as a K2 launch
+      cudaStream_t s = ctx->stream;
+      if (!fuse_flags.p) {
+        fuse_flags.alloc(static_cast<std::size_t>(E + 1) / 2);  // E unsigned flags
+        fuse_flags.zero(s);
+        fuse_ticket.alloc(1);  // one unsigned long long
+        fuse_ticket.zero(s);
+      }
+      exchange_halo(a.u);
+      SemArgs f = a;
+      f.e_begin = 0, f.e_end = E;
+      f.flags = reinterpret_cast<unsigned*>(fuse_flags.p);
+      f.ticket = reinterpret_cast<unsigned long long*>(fuse_ticket.p);
+      f.ticket_base = fuse_ticket_total;
+      f.epoch = ++fuse_epoch;
+      f.defer_top = distributed() && up() >= 0;
+      static const int fmode = [] {
+        const char* env = std::getenv("CMG_FUSED_MODE");
+        return env ? std::atoi(env) : 0;
+      }();
+      f.fuse_mode = fmode;
+      if (!sem_step_fused(f, epi, s)) fail(CMG_ERUNTIME, "sem: no fused kernel for this order");
+      fuse_ticket_total += static_cast<unsigned long long>(E);
+      if (distributed()) {
+        exchange_contrib();
+        if (f.defer_top) {
+          SemArgs top = a;
+          top.e_begin = E - static_cast<long>(Ex) * Ey, top.e_end = E;
+          sem_k2(top, epi, s);
+        }
+      }
+      return;
+    }
+    if (!distributed() || Ezl < 2 || !overlap) {
+      if (mode == SEM_AX) exchange_halo(a.u);
+      sem_k1(a, mode, epi, ctx->stream);
+      exchange_contrib();
+      sem_k2(a, epi, ctx->stream);
+      return;
+    }
+    // Partitioned: both face exchanges run on the communicator's side stream,
+    // hidden behind element work that does not need them --
+    //   input halo   || K1 on layers 1..Ezl-1  (only layer 0 reads the halo)
+    //   contributions || K2 on layers 0..Ezl-2 (only the top layer reads them)
+    cudaStream_t s = ctx->stream;
+    Comm& cm = *ctx->comm;
+    const long LE = static_cast<long>(Ex) * Ey;
+    SemArgs lo = a, hi = a;
+    lo.e_begin = 0, lo.e_end = LE;
+    hi.e_begin = LE, hi.e_end = E;
+    if (mode == SEM_AX) {
+      sem_pack_top(a, a.u, halo_send.p, s);
+      CMG_CUDA(cudaEventRecord(cm.ev_ready, s));
+      CMG_CUDA(cudaStreamWaitEvent(cm.side, cm.ev_ready, 0));
+      cm.sendrecv(halo_send.p, halo_send.n, halo_lo.p, halo_lo.n, up(), down(), cm.side);
+      CMG_CUDA(cudaEventRecord(cm.ev_halo, cm.side));
+    }
+    sem_k1(hi, mode, epi, s);
+    if (mode == SEM_AX) CMG_CUDA(cudaStreamWaitEvent(s, cm.ev_halo, 0));
+    sem_k1(lo, mode, epi, s);
+    sem_pack_contrib_bottom(a, contrib_send.p, s);
+    CMG_CUDA(cudaEventRecord(cm.ev_ready, s));
+    CMG_CUDA(cudaStreamWaitEvent(cm.side, cm.ev_ready, 0));
+    cm.sendrecv(contrib_send.p, contrib_send.n, contrib_hi.p, contrib_hi.n, down(), up(), cm.side);
+    CMG_CUDA(cudaEventRecord(cm.ev_contrib, cm.side));
+    SemArgs below = a, top = a;
+    below.e_begin = 0, below.e_end = E - LE;
+    top.e_begin = E - LE, top.e_end = E;
+    sem_k2(below, epi, s);
+    CMG_CUDA(cudaStreamWaitEvent(s, cm.ev_contrib, 0));
+    sem_k2(top, epi, s);
   }
 
   void apply(const double* x, double* y) override {
@@ -390,6 +475,22 @@ struct SemLevel final : cmg_op {
   void norm2(const double* a, double* out) override { layer_reduce(a, 0, 1, a, out, true); }
   void mdot(const double* V, std::size_t ldv, int nv, const double* w, double* out) override {
     layer_reduce(V, ldv, nv, w, out, false);
+  }
+  void cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coef_in, double* w, double* out,
+                double* hcol, int hstride) override {
+    if (nv > 32) {
+      launch_cgs_update(V, ldv, nv, coef_in, w, len, hcol, hstride, ctx->stream);
+      layer_reduce(V, ldv, nv, w, out, false);
+      return;
+    }
+    const long layer_len = static_cast<long>(Ex) * Ey * sem_nos(N);
+    sem_layer_cgs_dots(V, ldv, nv, coef_in, w, layer_len, Ezl, hcol, hstride, lpart.p, lout.p, ctx->stream);
+    const double* g = lout.p;
+    if (distributed()) {
+      ctx->comm->allgather(lout.p, lgath.p, static_cast<std::size_t>(nv) * Ezl, ctx->stream);
+      g = lgath.p;
+    }
+    sem_layer_finalize(g, nv, lpr.p, desc.nranks, out, 0, ctx->stream);
   }
 
   std::vector<long> slot_map() const {

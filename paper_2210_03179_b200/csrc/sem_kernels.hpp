@@ -63,8 +63,18 @@ struct SemArgs {
   double beta_last = 0;  // > 0: last sweep step, final x += beta_k d' fused, r/d' not stored
   int x_zero = 0;
   const int* k2tab = nullptr;  // K2 contributor table [nshared][K2TAB_STRIDE] (sem.cpp)
-  // element range [e_begin, e_end) processed by this launch (for overlap splits)
+  // element range [e_begin, e_end) processed by this launch (for overlap splits;
+  // K2 needs whole element layers)
   long e_begin = 0, e_end = 0;
+  int k2_z0 = 0;  // first local layer of a K2 launch (set by the launcher)
+  // fused step (sem_step_fused): elements claimed in decreasing order through
+  // *ticket (minus ticket_base), per-element "shell written" flags = epoch
+  unsigned* flags = nullptr;
+  unsigned long long* ticket = nullptr;
+  unsigned long long ticket_base = 0;
+  unsigned epoch = 0;
+  int defer_top = 0;  // top layer's shared nodes wait for the NCCL halo (K2 after the exchange)
+  int fuse_mode = 0;  // A/B knob (CMG_FUSED_MODE)
 };
 
 // upload the order-N GLL derivative matrix to constant memory (once per order)
@@ -72,6 +82,9 @@ void sem_set_derivative(int N, const double* D_host);
 // K1 over elements [e_begin, e_end) and K2 over the same elements
 void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s);
 void sem_k2(const SemArgs& a, int epi, cudaStream_t s);
+// K1 + K2 as one launch over [e_begin, e_end) (orders 5 and 7, AX mode);
+// false when the order has no fused kernel
+bool sem_step_fused(const SemArgs& a, int epi, cudaStream_t s);
 
 // pointwise epilogues over all slots (x_is_zero smoother inits)
 void sem_cheb4_init_zero(std::size_t n, const double* b, const double* invd, double c0, double* r,
@@ -114,6 +127,9 @@ void sem_restrict_local(const SemArgs& fine, int Nc, const double* J, const doub
 // per-layer partial inner products: out[v*Ezl + l] = sum over layer l of V_v . w
 void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
                     int nlayers, double* partials, double* out, cudaStream_t s);
+// fused CGS pass (nv <= 32): w -= V coef, hcol += coef, then the per-layer V^T w
+void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* coef, double* w, long layer_len,
+                        int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s);
 // final sum over all global layers (gathered [rank][v][layer_local] blocks) in z order
 void sem_layer_finalize(const double* gathered, int nv, const int* layers_per_rank, int nranks,
                         double* out, int do_sqrt, cudaStream_t s);

@@ -322,7 +322,9 @@ def test_sweep_csv_matches_reference_sweep(cm, tmp_path):
             b.iterations, b.fine_matvecs, b.converged, b.lambda_min_mult), a.case_id
         # power-iteration norms are tree-reduced on the device: lambda_tilde to rounding
         assert abs(a.lambda_tilde - b.lambda_tilde) <= 1e-13 * b.lambda_tilde
-        assert abs(a.rho - b.rho) <= 1e-9 * b.rho
+        # rho = (h_N/h_0)^(1/N): the histories agree to 1e-10 h_0, i.e. h_N only to
+        # ~1e-10 h_0/h_N ~ 1e-2 relative at tol 1e-8, divided by N in rho
+        assert abs(a.rho - b.rho) <= 1e-6 * b.rho
         assert abs(a.C_est - b.C_est) <= 1e-9 * b.C_est
         assert a.time_ms is None
     # best row per (Lx, factor): fewest matvecs, then iterations, then k
