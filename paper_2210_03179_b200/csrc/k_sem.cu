@@ -325,8 +325,14 @@ constexpr int k2_eb(int N) { return sem_nshared(N) >= 256 ? 1 : 256 / sem_nshare
 
 // One owned shared node: sum its <= 8 shell contributions in the fixed
 // (dz, dy, dx) order, then the step's epilogue.  CG: read the shell through L2
-// only (the fused step reads contributions its neighbours wrote in the same
-// launch).  Returns without work for padding slots.
+// only (for a caller that reads contributions written in the same launch).
+// Returns without work for padding slots.
+//
+// A single-launch step that ran this per owned node inside the element kernel
+// (elements claimed in decreasing order, per-element "shell written" flags)
+// was measured at E=64^3: 21.9 vs 34.1 GDOF-step/s for the K1 + K2 pair --
+// waiting for the +x neighbour's flag cost 1.15 ms and the in-block node work
+// 0.7 ms per step, against 0.47 ms for the separate K2 launch.
 template <int N, int EPI, bool CG>
 __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey, int ez, int s) {
   constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N);
@@ -436,150 +442,6 @@ void launch_k2(const SemArgs& a, cudaStream_t s) {
   const dim3 grid((unsigned)((a.Ex + k2_eb(N) - 1) / k2_eb(N)), (unsigned)a.Ey, (unsigned)(ne / per_layer));
   k_sem_k2<N, EPI><<<grid, k2_eb(N) * sem_nshared(N), 0, s>>>(b);
   CMG_LAUNCH_CHECK();
-}
-
-// ---------------------------------------------------------------- fused step (K1 + K2 in one launch)
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// One element per block, claimed in DECREASING index order through an atomic
-// ticket.  After the element kernel (the k_sem_k1_greg phases) the block
-// publishes "my shell contributions are written" (per-element flag = epoch)
-// and then finishes its own shared nodes itself: their other contributors are
-// its +x/+y/+z neighbours, which have larger indices, hence earlier tickets --
-// they are resident or finished, so the wait cannot deadlock -- and their
-// contributions come back from L2 moments after being written.  The separate
-// K2 launch, the HBM round trip of the shell buffer and one kernel boundary
-// per step disappear; the sums keep K2's fixed (dz, dy, dx) order, so results
-// are bitwise those of the two-kernel path.
-template <int N, int EPI, int KS, int MINB>
-__global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_step_fused(SemArgs A) {
-  using L = K1L<N, EPI, KS>;
-  using S = K3Smem<N, EPI, false>;
-  constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOPS = S::NOPS, NIP = S::NIP, KH = L::KH;
-  constexpr int NSH = sem_nshared(N);
-  constexpr bool HAS_OPS = NOPS > 0 && sem_nint(N) > 0;
-  static_assert(NSH <= N1 * N1 * KS, "one thread per owned shared node");
-  extern __shared__ __align__(128) double sm[];
-  __shared__ long e_claim;
-  double* so = sm + S::o_off;
-  double* su = sm + S::u_off;
-  double* sr = sm + S::r_off;
-  double* ss = sm + S::s_off;
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
-  const int t = threadIdx.x;
-  if (t == 0)
-    e_claim = A.e_end - 1 -
-              (A.fuse_mode == 0 ? (long)(atomicAdd(A.ticket, 1ull) - A.ticket_base) : (long)blockIdx.x);
-  __syncthreads();
-  const long e = e_claim;
-  const int line = t % (N1 * N1);
-  const int h = t / (N1 * N1);
-  const int ta = line % N1, tb = line / N1;
-  if constexpr (HAS_OPS) {
-    if (t == 0) {
-      const bool skip_x = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) && A.x_zero;
-      mbar_init(bar, 1);
-      mbar_expect_tx(bar, (NOPS - (skip_x ? 1 : 0)) * NIP * 8);
-#pragma unroll
-      for (int op = 0; op < NOPS; ++op) {
-        if (op == 0 && skip_x) continue;
-        bulk_g2s(so + (std::size_t)op * NIP, epi_op<EPI>(A, op) + e * sem_nos(N), NIP * 8, bar);
-      }
-    }
-  }
-  const double* Ge = A.G + e * 6 * NP;
-  double wt[KH], dvh[KH];
-#define ON_PART(fn, ...)                                   \
-  do {                                                     \
-    switch (h) {                                           \
-      case 0: L::template fn<0>(__VA_ARGS__); break;       \
-      case 1: L::template fn<1 % KS>(__VA_ARGS__); break;  \
-      case 2: L::template fn<2 % KS>(__VA_ARGS__); break;  \
-      default: L::template fn<3 % KS>(__VA_ARGS__); break; \
-    }                                                      \
-  } while (0)
-  ON_PART(gather, A, su, ta, tb, e);
-  __syncthreads();
-  ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
-  __syncthreads();
-  ON_PART(geometry_reg, Ge, sr, ss, ta, tb, wt);
-  __syncthreads();
-  ON_PART(div_r, sr, su, ta, tb);
-  __syncthreads();
-  ON_PART(div_s, ss, su, sr, ta, tb, wt);
-  __syncthreads();
-  if constexpr (HAS_OPS) mbar_wait(bar, 0);
-  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
-#undef ON_PART
-  if (A.fuse_mode <= 1) __threadfence();  // this thread's shell stores, device-visible
-  __syncthreads();
-  if (t == 0) {
-    if (A.fuse_mode >= 2) __threadfence();  // block's stores ordered by the barrier (cumulative)
-    st_release_u32(A.flags + e, A.epoch);
-  }
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
-  if (A.defer_top && ez == A.Ezl - 1) return;  // uniform: K2 after the halo exchange
-  if (A.fuse_mode == 3) return;                 // timing probe only (no shared-node work)
-  if (A.fuse_mode == 5) {
-    // probe: shared-node work without waiting (wrong results)
-  } else if (A.fuse_mode <= 1 || A.fuse_mode == 4) {
-    if (t >= 1 && t < 8) {
-      const int dx = t & 1, dy = (t >> 1) & 1, dz = t >> 2;
-      if (ex + dx < A.Ex && ey + dy < A.Ey && ez + dz < A.Ezl) {
-        const unsigned* f = A.flags + e + dx + (long)A.Ex * (dy + (long)A.Ey * dz);
-        while (ld_acquire_u32(f) != A.epoch) __nanosleep(32);
-      }
-    }
-  } else if (t == 0) {
-    for (int q = 1; q < 8; ++q) {
-      const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
-      if (ex + dx < A.Ex && ey + dy < A.Ey && ez + dz < A.Ezl) {
-        const unsigned* f = A.flags + e + dx + (long)A.Ex * (dy + (long)A.Ey * dz);
-        while (ld_acquire_u32(f) != A.epoch) __nanosleep(200);
-      }
-    }
-  }
-  __syncthreads();
-  if (A.fuse_mode == 4) return;  // probe: wait only (wrong results)
-  if (t < NSH) k2_node<N, EPI, true>(A, e, ex, ey, ez, t);
-}
-
-template <int N, int EPI>
-void launch_fused(const SemArgs& a, cudaStream_t s) {
-  const long ne = a.e_end - a.e_begin;
-  if (ne <= 0) return;
-  constexpr std::size_t smem = K3Smem<N, EPI, false>::bytes;
-  static bool configured = false;
-  if (!configured) {
-    CMG_CUDA(cudaFuncSetAttribute(k_sem_step_fused<N, EPI, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    configured = true;
-  }
-  k_sem_step_fused<N, EPI, 2, 8><<<(unsigned)ne, (N + 1) * (N + 1) * 2, smem, s>>>(a);
-  CMG_LAUNCH_CHECK();
-}
-
-template <int N>
-bool dispatch_fused(const SemArgs& a, int epi, cudaStream_t s) {
-  if constexpr (N >= 5 && (N + 1) % 2 == 0) {
-    switch (epi) {
-      case EPI_STORE: launch_fused<N, EPI_STORE>(a, s); return true;
-      case EPI_ADD: launch_fused<N, EPI_ADD>(a, s); return true;
-      case EPI_RESID: launch_fused<N, EPI_RESID>(a, s); return true;
-      case EPI_CHEB4: launch_fused<N, EPI_CHEB4>(a, s); return true;
-      case EPI_CHEB1: launch_fused<N, EPI_CHEB1>(a, s); return true;
-      case EPI_CHEB4_INIT: launch_fused<N, EPI_CHEB4_INIT>(a, s); return true;
-      case EPI_CHEB1_INIT: launch_fused<N, EPI_CHEB1_INIT>(a, s); return true;
-    }
-  }
-  return false;
 }
 
 template <int N, int MODE>
@@ -1035,13 +897,6 @@ void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
   CMG_ORDERS(X)
 #undef X
   throw Error(EINVAL_, "SEM order must be one of 1,2,3,4,5,7");
-}
-
-bool sem_step_fused(const SemArgs& a, int epi, cudaStream_t s) {
-#define X(n) if (a.N == n) return dispatch_fused<n>(a, epi, s);
-  CMG_ORDERS(X)
-#undef X
-  return false;
 }
 
 void sem_k2(const SemArgs& a, int epi, cudaStream_t s) {

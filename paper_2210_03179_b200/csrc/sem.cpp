@@ -97,9 +97,6 @@ struct SemLevel final : cmg_op {
   int nshell = 0, nshared = 0;
   DBuf G, Dm, xi, w, shell, halo_lo, halo_send, contrib_hi, contrib_send, diagv, mask, Lrhs;
   DBuf lpart, lout, lgath;
-  DBuf fuse_flags, fuse_ticket;  // fused step: per-element epoch flags, element ticket
-  unsigned fuse_epoch = 0;
-  unsigned long long fuse_ticket_total = 0;
   IBuf lut, shared, lpr, k2tab;
   std::vector<int> lpr_h;
 
@@ -289,46 +286,6 @@ struct SemLevel final : cmg_op {
       const char* env = std::getenv("CMG_SEM_OVERLAP");
       return env && std::atoi(env) == 1;
     }();
-    static const bool fused = [] {  // experimental single-launch step, opt-in
-      const char* env = std::getenv("CMG_SEM_FUSED");
-      return env && std::atoi(env) == 1;
-    }();
-    if (mode == SEM_AX && fused && (N == 5 || N == 7)) {
-      // one launch per operator application (k_sem_step_fused); partitioned:
-      // input halo first, bottom-face contributions down after, then the top
-      // layer's shared nodes (the only ones needing them) as a K2 launch
-      cudaStream_t s = ctx->stream;
-      if (!fuse_flags.p) {
-        fuse_flags.alloc(static_cast<std::size_t>(E + 1) / 2);  // E unsigned flags
-        fuse_flags.zero(s);
-        fuse_ticket.alloc(1);  // one unsigned long long
-        fuse_ticket.zero(s);
-      }
-      exchange_halo(a.u);
-      SemArgs f = a;
-      f.e_begin = 0, f.e_end = E;
-      f.flags = reinterpret_cast<unsigned*>(fuse_flags.p);
-      f.ticket = reinterpret_cast<unsigned long long*>(fuse_ticket.p);
-      f.ticket_base = fuse_ticket_total;
-      f.epoch = ++fuse_epoch;
-      f.defer_top = distributed() && up() >= 0;
-      static const int fmode = [] {
-        const char* env = std::getenv("CMG_FUSED_MODE");
-        return env ? std::atoi(env) : 0;
-      }();
-      f.fuse_mode = fmode;
-      if (!sem_step_fused(f, epi, s)) fail(CMG_ERUNTIME, "sem: no fused kernel for this order");
-      fuse_ticket_total += static_cast<unsigned long long>(E);
-      if (distributed()) {
-        exchange_contrib();
-        if (f.defer_top) {
-          SemArgs top = a;
-          top.e_begin = E - static_cast<long>(Ex) * Ey, top.e_end = E;
-          sem_k2(top, epi, s);
-        }
-      }
-      return;
-    }
     if (!distributed() || Ezl < 2 || !overlap) {
       if (mode == SEM_AX) exchange_halo(a.u);
       sem_k1(a, mode, epi, ctx->stream);

@@ -67,14 +67,6 @@ struct SemArgs {
   // K2 needs whole element layers)
   long e_begin = 0, e_end = 0;
   int k2_z0 = 0;  // first local layer of a K2 launch (set by the launcher)
-  // fused step (sem_step_fused): elements claimed in decreasing order through
-  // *ticket (minus ticket_base), per-element "shell written" flags = epoch
-  unsigned* flags = nullptr;
-  unsigned long long* ticket = nullptr;
-  unsigned long long ticket_base = 0;
-  unsigned epoch = 0;
-  int defer_top = 0;  // top layer's shared nodes wait for the NCCL halo (K2 after the exchange)
-  int fuse_mode = 0;  // A/B knob (CMG_FUSED_MODE)
 };
 
 // upload the order-N GLL derivative matrix to constant memory (once per order)
@@ -82,9 +74,6 @@ void sem_set_derivative(int N, const double* D_host);
 // K1 over elements [e_begin, e_end) and K2 over the same elements
 void sem_k1(const SemArgs& a, int mode, int epi, cudaStream_t s);
 void sem_k2(const SemArgs& a, int epi, cudaStream_t s);
-// K1 + K2 as one launch over [e_begin, e_end) (orders 5 and 7, AX mode);
-// false when the order has no fused kernel
-bool sem_step_fused(const SemArgs& a, int epi, cudaStream_t s);
 
 // pointwise epilogues over all slots (x_is_zero smoother inits)
 void sem_cheb4_init_zero(std::size_t n, const double* b, const double* invd, double c0, double* r,
