@@ -48,7 +48,35 @@ class Clocks:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            try:
+                p = torch.cuda.get_device_properties(self.device)
+                bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
+        except Exception:
+            return None, None
+
     def _run(self):
+        nv, h = self._nvml_handle()
+        if h is not None:  # NVML: a sample every 5 ms inside the timed region
+            bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                    ("sw_power_cap", 0x4)]
+            try:
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                while not self._stop.is_set():
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for _, b in bits])
+                    self._stop.wait(0.005)
+                return
+            except Exception:
+                self.samples = []
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
