@@ -100,6 +100,13 @@ class Clocks:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if not self.samples:  # region shorter than one poll: one sample at its end
+            self._stop.clear()
+            t = threading.Thread(target=self._run, daemon=True)
+            t.start()
+            time.sleep(0.05)
+            self._stop.set()
+            t.join(timeout=10)
 
     def summary(self):
         if not self.samples:

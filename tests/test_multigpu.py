@@ -71,3 +71,17 @@ def test_sweep_across_ranks_matches_single_gpu(tmp_path):
     a = (out1 / "sweep.csv").read_text()
     b = (out2 / "sweep.csv").read_text()
     assert a == b and a.count("\n") == 1 + 3 * 2 * 2 * 2 * 2
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_full_size_partition_identity(tmp_path):
+    """BASELINE configs[4] at full size (N=7, E=64^3, 89.3M unknowns), the bench's
+    (8,0) 4th-kind p-MG PGMRES solve: residual history, iteration count and a
+    sha256 of the whole canonical solution are identical at 1, 2 (and 4) GPUs."""
+    extra = ("--E", "64", "--ez", "64", "--kpre", "8", "--hash-only")
+    r1 = _run(1, str(tmp_path / "f1.json"), extra)
+    assert r1["iterations"] == 9
+    for w in [2] + ([4] if _ngpus() >= 4 else []):
+        rw = _run(w, str(tmp_path / f"f{w}.json"), extra)
+        for k in ("iterations", "fine_matvecs", "history", "lambda", "x_sha256"):
+            assert rw[k] == r1[k], (w, k)

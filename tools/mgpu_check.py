@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--ez", type=int, default=8)
     ap.add_argument("--geometry", type=int, default=0)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--hash-only", action="store_true", help="write a sha256 of x instead of x itself")
+    ap.add_argument("--kpre", type=int, default=4)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -48,7 +50,7 @@ def main():
     d = sem.SemDesc(7, args.E, args.E, args.ez, geometry=args.geometry, eps=0.3, rank=rank, nranks=world)
     P = sem.PMGHierarchy(d, (7, 3, 1), ctx=ctx)
     b = P.A.rhs()
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 4, 0)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), args.kpre, 0)
     x, rep = cm.pgmres(P.A, P.preconditioner(cyc), b, None, cm.SolveOptions(tol=1e-8))
     # gather the canonical solution on rank 0
     xc = P.A.to_canonical(x)
@@ -62,9 +64,14 @@ def main():
                "lambda": [float(v).hex() for v in P.lambda_tilde],
                "x_norm": float(np.linalg.norm(xc)).hex(), "x_sum": float(np.sum(xc)).hex(),
                "x_sample": [float(v).hex() for v in xc[:: max(1, xc.size // 64)]]}
+        if args.hash_only:
+            import hashlib
+
+            res["x_sha256"] = hashlib.sha256(np.ascontiguousarray(xc).tobytes()).hexdigest()
         with open(args.out, "w") as fh:
             json.dump(res, fh)
-        np.save(args.out + ".x.npy", xc)
+        if not args.hash_only:
+            np.save(args.out + ".x.npy", xc)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
