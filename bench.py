@@ -54,6 +54,8 @@ class Clocks:
 
             pynvml.nvmlInit()
             try:
+                import torch
+
                 p = torch.cuda.get_device_properties(self.device)
                 bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
                 return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
@@ -179,7 +181,7 @@ def run_reference_arm(args):
     cores = os.cpu_count() or 1
     E = args.cpu_E
     order = 8
-    reps = 3
+    reps = max(1, args.steps)  # timed sweeps per replica (capped at 20 s each)
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(cores) as pool:
         outs = pool.map(_replica, [(E, order, reps)] * cores)
@@ -188,7 +190,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": "GDOF/s per Chebyshev smoother sweep", "value": value,
         "unit": "GDOF-step/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"SEM Poisson box N=7 E={E}^3 4th-kind Chebyshev-Jacobi sweep "
                                                     f"order 8 (bounded CPU sample of the E=64^3 workload)"},
         "cpu_baseline": {"value": value, "unit": "GDOF-step/s", "cores": cores, "kind": outs[0][1],
