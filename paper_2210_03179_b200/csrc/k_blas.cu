@@ -190,31 +190,32 @@ __global__ void k_cgs_update(const double* __restrict__ V, std::size_t ldv, int 
 // sums of V^T w_new with k_mdot_partials' grid/block/reduction structure, so
 // the coefficients are bit-identical to the unfused pair while V is streamed
 // from HBM once instead of twice (the second read of each V_li hits cache).
+template <int MAXV>
 __global__ void __launch_bounds__(kRedThreads) k_cgs_mdot(const double* __restrict__ V, std::size_t ldv,
                                                           int nv, const double* __restrict__ coef,
                                                           double* __restrict__ w, std::size_t n, double* hcol,
                                                           int hstride, double* __restrict__ partials) {
-  __shared__ double c[kCgsFuseMax];
-  __shared__ double sh[kCgsFuseMax][kRedThreads / 32];
+  __shared__ double c[MAXV];
+  __shared__ double sh[MAXV][kRedThreads / 32];
   for (int l = threadIdx.x; l < nv; l += blockDim.x) c[l] = coef[l];
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0)
     for (int l = 0; l < nv; ++l) hcol[(std::size_t)l * hstride] += c[l];
-  double acc[kCgsFuseMax];
+  double acc[MAXV];
 #pragma unroll
-  for (int q = 0; q < kCgsFuseMax; ++q) acc[q] = 0.0;
+  for (int q = 0; q < MAXV; ++q) acc[q] = 0.0;
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
        i += (std::size_t)gridDim.x * blockDim.x) {
     double v = w[i];
     for (int l = 0; l < nv; ++l) v += -c[l] * V[(std::size_t)l * ldv + i];
     w[i] = v;
 #pragma unroll
-    for (int q = 0; q < kCgsFuseMax; ++q)
+    for (int q = 0; q < MAXV; ++q)
       if (q < nv) acc[q] += V[(std::size_t)q * ldv + i] * v;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int q = 0; q < kCgsFuseMax; ++q) {
+  for (int q = 0; q < MAXV; ++q) {
     if (q < nv) {
       const double s = warp_sum(acc[q]);
       if (lane == 0) sh[q][warp] = s;
@@ -443,7 +444,9 @@ void launch_cgs_update(const double* V, std::size_t ldv, int nv, const double* c
 void launch_cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coef, double* w, std::size_t n,
                     double* hcol, int hstride, double* partials, double* out, cudaStream_t s) {
   const int g = red_grid(n);
-  k_cgs_mdot<<<g, kRedThreads, 0, s>>>(V, ldv, nv, coef, w, n, hcol, hstride, partials);
+  if (nv <= 8) k_cgs_mdot<8><<<g, kRedThreads, 0, s>>>(V, ldv, nv, coef, w, n, hcol, hstride, partials);
+  else if (nv <= 16) k_cgs_mdot<16><<<g, kRedThreads, 0, s>>>(V, ldv, nv, coef, w, n, hcol, hstride, partials);
+  else k_cgs_mdot<32><<<g, kRedThreads, 0, s>>>(V, ldv, nv, coef, w, n, hcol, hstride, partials);
   CMG_LAUNCH_CHECK();
   k_finalize<<<nv, kRedThreads, 0, s>>>(partials, g, out, 0, nv);
   CMG_LAUNCH_CHECK();

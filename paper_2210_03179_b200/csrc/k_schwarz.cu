@@ -17,21 +17,25 @@ __device__ __forceinline__ int owner1d_s(int g, int ne, int& oe) {
 }
 
 // one block per element: gather r on the extended box, FDM solve, write the
-// local solution (RAS: the element's own (N+1)^3 nodes; ASM: all (N+3)^3)
+// local solution (RAS: the element's own (N+1)^3 nodes; ASM: all (N+3)^3).
+// Each mode product is a set of line contractions: a thread loads one
+// (N+3)-line of the box into registers once and produces the whole output
+// line, with the 1D eigenbasis rows broadcast from shared memory (every
+// output still sums its N+3 terms in ascending order).
 template <int N>
-__global__ void k_schwarz_local(SchwarzArgs A) {
-  constexpr int PB = N + 3, PB3 = PB * PB * PB, N1 = N + 1, NOS = sem_nos(N);
+__global__ void __launch_bounds__(128) k_schwarz_local(SchwarzArgs A) {
+  constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, N1 = N + 1, NOS = sem_nos(N);
   __shared__ double u[PB3], t[PB3];
-  __shared__ double S[3][PB * PB], lam[3][PB];
+  __shared__ double S[3][PB2], lam[3][PB];
   const long e = blockIdx.x;
   const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
   for (int d = 0; d < 3; ++d) {
     const int id = A.sidx[e * 3 + d];
-    for (int q = threadIdx.x; q < PB * PB; q += blockDim.x) S[d][q] = A.S[(long)id * PB * PB + q];
+    for (int q = threadIdx.x; q < PB2; q += blockDim.x) S[d][q] = A.S[(long)id * PB2 + q];
     for (int q = threadIdx.x; q < PB; q += blockDim.x) lam[d][q] = A.lam[(long)id * PB + q];
   }
   for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
-    const int a = q % PB, b = (q / PB) % PB, c = q / (PB * PB);
+    const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
     int oex = 0, oey = 0, oez = 0;
     const int ax = owner1d_s<N>(ex * N + a - 1, A.Ex, oex);
     const int ay = owner1d_s<N>(ey * N + b - 1, A.Ey, oey);
@@ -42,40 +46,55 @@ __global__ void k_schwarz_local(SchwarzArgs A) {
     u[q] = v;
   }
   __syncthreads();
-  // forward: (Sz^T x Sy^T x Sx^T) u, one dimension at a time
+  // line l of dimension dim: the other two indices (p, q) = (l % PB, l / PB)
+  auto line_base = [](int dim, int l) {
+    const int p = l % PB, q = l / PB;
+    return dim == 0 ? PB * (p + PB * q) : (dim == 1 ? p + PB2 * q : p + PB * q);
+  };
+  constexpr int STRIDE[3] = {1, PB, PB2};
+  // forward: (Sz^T x Sy^T x Sx^T) u; the eigenvalue division fused into the last pass
   double* in = u;
   double* out = t;
+#pragma unroll 1
   for (int dim = 0; dim < 3; ++dim) {
-    for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
-      const int a = q % PB, b = (q / PB) % PB, c = q / (PB * PB);
-      const int o = dim == 0 ? a : (dim == 1 ? b : c);
-      const int base = q - o * (dim == 0 ? 1 : (dim == 1 ? PB : PB * PB));
-      const int st = dim == 0 ? 1 : (dim == 1 ? PB : PB * PB);
-      double v = 0.0;
+    for (int l = threadIdx.x; l < PB2; l += blockDim.x) {
+      const int base = line_base(dim, l), st = STRIDE[dim];
+      double v[PB];
 #pragma unroll
-      for (int m = 0; m < PB; ++m) v += S[dim][m * PB + o] * in[base + m * st];
-      out[q] = v;
+      for (int m = 0; m < PB; ++m) v[m] = in[base + m * st];
+#pragma unroll 2
+      for (int o = 0; o < PB; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < PB; ++m) acc += S[dim][m * PB + o] * v[m];
+        const int q = base + o * st;
+        if (dim == 2) {
+          const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
+          acc /= (lam[0][a] + lam[1][b] + lam[2][c]);
+        }
+        out[q] = acc;
+      }
     }
     __syncthreads();
     double* tmp = in;
     in = out;
     out = tmp;
   }
-  for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
-    const int a = q % PB, b = (q / PB) % PB, c = q / (PB * PB);
-    in[q] /= (lam[0][a] + lam[1][b] + lam[2][c]);
-  }
-  __syncthreads();
+  // backward: (Sz x Sy x Sx)
+#pragma unroll 1
   for (int dim = 0; dim < 3; ++dim) {
-    for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
-      const int a = q % PB, b = (q / PB) % PB, c = q / (PB * PB);
-      const int o = dim == 0 ? a : (dim == 1 ? b : c);
-      const int st = dim == 0 ? 1 : (dim == 1 ? PB : PB * PB);
-      const int base = q - o * st;
-      double v = 0.0;
+    for (int l = threadIdx.x; l < PB2; l += blockDim.x) {
+      const int base = line_base(dim, l), st = STRIDE[dim];
+      double v[PB];
 #pragma unroll
-      for (int m = 0; m < PB; ++m) v += S[dim][o * PB + m] * in[base + m * st];
-      out[q] = v;
+      for (int m = 0; m < PB; ++m) v[m] = in[base + m * st];
+#pragma unroll 2
+      for (int o = 0; o < PB; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < PB; ++m) acc += S[dim][o * PB + m] * v[m];
+        out[base + o * st] = acc;
+      }
     }
     __syncthreads();
     double* tmp = in;

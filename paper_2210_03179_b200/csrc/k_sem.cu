@@ -339,8 +339,8 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
   // host-built table (sem.cpp, L1-resident): [count, a|b<<8|c<<16, (offset, dx|dy<<1|dz<<2) x count],
   // offset = shell position relative to this element's shell block
   const int* tab = A.k2tab + s * K2TAB_STRIDE;
-  const int n = __ldg(tab), abc = __ldg(tab + 1);
-  const int a = abc & 0xff, b = (abc >> 8) & 0xff, c = abc >> 16;
+  const int head = __ldg(tab);
+  const int n = head & 0xff, a = (head >> 8) & 0xff, b = (head >> 16) & 0xff, c = head >> 24;
   // padding (far domain boundary) is not an unknown
   if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
   const double* sh = A.shell + e * A.nshell;
@@ -349,7 +349,8 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
 #pragma unroll
   for (int cidx = 0; cidx < 8; ++cidx) {
     if (cidx < n) {
-      const int off = __ldg(tab + 2 + 2 * cidx), f = __ldg(tab + 3 + 2 * cidx);
+      const int p = __ldg(tab + 1 + cidx);
+      const int off = p & 0x0fffffff, f = (unsigned)p >> 28;
       if (top && (f & 4)) {
         // halo: k=0 face of the layer above, indexed by (ex', ey', i', j')
         const int dx = f & 1, dy = (f >> 1) & 1;
@@ -820,11 +821,13 @@ __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int 
 // arithmetic) and the per-layer partials of V^T w_new with k_layer_dots' exact
 // chunking and reduction order -- coefficients are bit-identical to the
 // unfused update + layer dots, V is streamed from HBM once.
+// MAXV: compile-time bound on nv (8/16/32) so the accumulators of short bases
+// do not cost the registers of long ones.
+template <int MAXV>
 __global__ void __launch_bounds__(256) k_layer_cgs_dots(const double* __restrict__ V, std::size_t ldv, int nv,
                                                         const double* __restrict__ coef, double* __restrict__ w,
                                                         long layer_len, int nlayers, double* hcol, int hstride,
                                                         double* __restrict__ partials) {
-  constexpr int MAXV = 32;
   const int layer = blockIdx.y, chunk = blockIdx.x;
   __shared__ double c[MAXV];
   __shared__ double sh[MAXV][8];
@@ -1009,7 +1012,9 @@ void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, l
 void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* coef, double* w, long layer_len,
                         int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s) {
   dim3 grid(LCH, nlayers, 1);
-  k_layer_cgs_dots<<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  if (nv <= 8) k_layer_cgs_dots<8><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  else if (nv <= 16) k_layer_cgs_dots<16><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  else k_layer_cgs_dots<32><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   CMG_LAUNCH_CHECK();
   const long t = (long)nv * nlayers;
   k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);

@@ -128,7 +128,16 @@ struct SemLevel final : cmg_op {
     // own shared slots in slot order.
     std::vector<int> lut_h(NP, -1), sh_h;
     nshell = 0;
-    {
+    static const bool lex_shell = [] {
+      const char* env = std::getenv("CMG_SHELL_LEX");
+      return env && std::atoi(env) == 1;
+    }();
+    if (lex_shell) {  // lexicographic shell order (A/B knob)
+      for (int k = 0; k < N1; ++k)
+        for (int j = 0; j < N1; ++j)
+          for (int i = 0; i < N1; ++i)
+            if (!(i >= 1 && i < N && j >= 1 && j < N && k >= 1 && k < N)) lut_h[(k * N1 + j) * N1 + i] = nshell++;
+    } else {
       const int nsh = sem_nshared(N);
       for (int dz = 0; dz < 2; ++dz)
         for (int dy = 0; dy < 2; ++dy)
@@ -161,22 +170,20 @@ struct SemLevel final : cmg_op {
         int a2, b2, c2;
         sem_shared_abc(N, s2, a2, b2, c2);
         int* row = tab.data() + static_cast<std::size_t>(s2) * K2TAB_STRIDE;
-        row[1] = a2 | (b2 << 8) | (c2 << 16);
         const int i = a2 + 1, j = b2 + 1, k = c2 + 1;
-        if (i > N || j > N || k > N) continue;  // pad slot: no contributions
         int cnt = 0;
-        for (int dz = 0; dz < (k == N ? 2 : 1); ++dz)
-          for (int dy = 0; dy < (j == N ? 2 : 1); ++dy)
-            for (int dx = 0; dx < (i == N ? 2 : 1); ++dx) {
-              const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
-              const long off = (dx + static_cast<long>(Ex) * (dy + static_cast<long>(Ey) * dz)) * nshell +
-                               lut_h[(lk * N1 + lj) * N1 + li];
-              if (off > 0x7fffffffL) fail(CMG_EINVAL, "sem: element rows too long for the K2 table");
-              row[2 + 2 * cnt] = static_cast<int>(off);
-              row[3 + 2 * cnt] = dx | (dy << 1) | (dz << 2);
-              ++cnt;
-            }
-        row[0] = cnt;
+        if (i <= N && j <= N && k <= N) {  // the pad slot has no contributions
+          for (int dz = 0; dz < (k == N ? 2 : 1); ++dz)
+            for (int dy = 0; dy < (j == N ? 2 : 1); ++dy)
+              for (int dx = 0; dx < (i == N ? 2 : 1); ++dx) {
+                const int li = i - dx * N, lj = j - dy * N, lk = k - dz * N;
+                const long off = (dx + static_cast<long>(Ex) * (dy + static_cast<long>(Ey) * dz)) * nshell +
+                                 lut_h[(lk * N1 + lj) * N1 + li];
+                if (off > 0x0fffffffL) fail(CMG_EINVAL, "sem: element rows too long for the K2 table");
+                row[1 + cnt++] = static_cast<int>(off) | ((dx | (dy << 1) | (dz << 2)) << 28);
+              }
+        }
+        row[0] = cnt | (a2 << 8) | (b2 << 16) | (c2 << 24);
       }
       k2tab.upload(tab);
     }

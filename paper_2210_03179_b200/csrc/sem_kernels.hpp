@@ -32,8 +32,9 @@ enum SemEpi : int {
   EPI_ADD = 6         // y += w
 };
 
-// K2 contributor table row: count, packed (a,b,c), then (shell offset, dx|dy<<1|dz<<2) x 8
-constexpr int K2TAB_STRIDE = 18;
+// K2 contributor table row: [count | a<<8 | b<<16 | c<<24], then per contribution
+// (shell offset relative to the owner's block) | (dx | dy<<1 | dz<<2) << 28
+constexpr int K2TAB_STRIDE = 9;
 
 struct SemArgs {
   int N = 7;

@@ -19,7 +19,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--case", default="sem", choices=["sem", "fd"])
+    ap.add_argument("--case", default="sem", choices=["sem", "fd", "ras"])
     ap.add_argument("--E", type=int, default=64)
     args = ap.parse_args()
     import torch
@@ -28,7 +28,12 @@ def main():
     from paper_2210_03179_b200 import sem
 
     ctx = cm.Context(0)
-    if args.case == "sem":
+    if args.case == "ras":  # configs[2]: Chebyshev-RAS (1,1), E=32^3
+        P = sem.PMGHierarchy(sem.SemDesc(7, 32, 32, 32), (7, 3, 1), smoother=sem.RAS, ctx=ctx)
+        A, b = P.A, P.A.rhs()
+        M = P.preconditioner(cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 1, 1))
+        opts = cm.SolveOptions(tol=1e-8, restart=30, maxit=500)
+    elif args.case == "sem":
         P = sem.PMGHierarchy(sem.SemDesc(7, args.E, args.E, args.E), (7, 3, 1), ctx=ctx)
         A, b = P.A, P.A.rhs()
         M = P.preconditioner(cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 8, 0))
