@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numbers>
 #include <string>
@@ -671,8 +672,16 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
       A->apply(Zj, w.p);
       // CGS(2) (krylov.hpp:186-195): project, subtract, [project again, subtract];
       // the first subtraction and the second projection share one pass over V
+      static const bool fuse_cgs = [] {
+        const char* env = std::getenv("CMG_CGS_FUSE");
+        return !(env && std::atoi(env) == 0);
+      }();
       A->mdot(V.p, L, j + 1, w.p, dsc + S_COEF);
-      if (o.reorthogonalize) {
+      if (o.reorthogonalize && !fuse_cgs) {
+        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF, w.p, L, H + j, m, s);
+        A->mdot(V.p, L, j + 1, w.p, dsc + S_COEF2);
+        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF2, w.p, L, H + j, m, s);
+      } else if (o.reorthogonalize) {
         A->cgs_mdot(V.p, L, j + 1, dsc + S_COEF, w.p, dsc + S_COEF2, H + j, m);
         launch_cgs_update(V.p, L, j + 1, dsc + S_COEF2, w.p, L, H + j, m, s);
       } else {

@@ -25,8 +25,12 @@ __device__ __forceinline__ int owner1d_s(int g, int ne, int& oe) {
 template <int N>
 __global__ void __launch_bounds__(128) k_schwarz_local(SchwarzArgs A) {
   constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, N1 = N + 1, NOS = sem_nos(N);
-  __shared__ double u[PB3], t[PB3];
-  __shared__ double S[3][PB2], lam[3][PB];
+  // box stored with an odd x pitch: lines along x (stride PX between threads)
+  // then hit distinct shared-memory banks
+  constexpr int PX = PB | 1, PS = PX * PB;
+  __shared__ double u[PS * PB], t[PS * PB];
+  __shared__ __align__(16) double S[3][PB2];
+  __shared__ double lam[3][PB];
   const long e = blockIdx.x;
   const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
   for (int d = 0; d < 3; ++d) {
@@ -43,36 +47,78 @@ __global__ void __launch_bounds__(128) k_schwarz_local(SchwarzArgs A) {
     double v = 0.0;
     if (ax >= 0 && ay >= 0 && az >= 0)
       v = A.r[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * oez)) * NOS + sem_pos(N, ax, ay, az)];
-    u[q] = v;
+    u[a + PX * b + PS * c] = v;
   }
   __syncthreads();
   // line l of dimension dim: the other two indices (p, q) = (l % PB, l / PB)
   auto line_base = [](int dim, int l) {
     const int p = l % PB, q = l / PB;
-    return dim == 0 ? PB * (p + PB * q) : (dim == 1 ? p + PB2 * q : p + PB * q);
+    return dim == 0 ? PX * p + PS * q : (dim == 1 ? p + PS * q : p + PX * q);
   };
-  constexpr int STRIDE[3] = {1, PB, PB2};
-  // forward: (Sz^T x Sy^T x Sx^T) u; the eigenvalue division fused into the last pass
+  constexpr int STRIDE[3] = {1, PX, PS};
+  // Two lines per thread share every eigenbasis load (the broadcast loads of
+  // S dominate the shared-memory traffic), and S is read two entries at a time
+  // when PB is even.  Every output still sums its PB terms in ascending order.
+  constexpr int HALF = (PB2 + 1) / 2;
+  constexpr bool PAIR = PB % 2 == 0;
   double* in = u;
   double* out = t;
+  // forward: (Sz^T x Sy^T x Sx^T) u; the eigenvalue division fused into the last pass
 #pragma unroll 1
   for (int dim = 0; dim < 3; ++dim) {
-    for (int l = threadIdx.x; l < PB2; l += blockDim.x) {
-      const int base = line_base(dim, l), st = STRIDE[dim];
-      double v[PB];
+    const double* Sd = S[dim];
+    for (int l = threadIdx.x; l < HALF; l += blockDim.x) {
+      const int l2 = l + HALF;
+      const bool two = l2 < PB2;
+      const int b1 = line_base(dim, l), b2 = line_base(dim, two ? l2 : l), st = STRIDE[dim];
+      double v1[PB], v2[PB];
 #pragma unroll
-      for (int m = 0; m < PB; ++m) v[m] = in[base + m * st];
-#pragma unroll 2
-      for (int o = 0; o < PB; ++o) {
-        double acc = 0.0;
+      for (int m = 0; m < PB; ++m) {
+        v1[m] = in[b1 + m * st];
+        v2[m] = in[b2 + m * st];
+      }
+      if constexpr (PAIR) {
+#pragma unroll 1
+        for (int o = 0; o < PB; o += 2) {
+          double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int m = 0; m < PB; ++m) acc += S[dim][m * PB + o] * v[m];
-        const int q = base + o * st;
-        if (dim == 2) {
-          const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
-          acc /= (lam[0][a] + lam[1][b] + lam[2][c]);
+          for (int m = 0; m < PB; ++m) {
+            const double2 sp = *reinterpret_cast<const double2*>(Sd + m * PB + o);
+            a0 += sp.x * v1[m];
+            a1 += sp.y * v1[m];
+            c0 += sp.x * v2[m];
+            c1 += sp.y * v2[m];
+          }
+          if (dim == 2) {
+            a0 /= (lam[0][l % PB] + lam[1][l / PB] + lam[2][o]);
+            a1 /= (lam[0][l % PB] + lam[1][l / PB] + lam[2][o + 1]);
+            c0 /= (lam[0][l2 % PB] + lam[1][l2 / PB] + lam[2][o]);
+            c1 /= (lam[0][l2 % PB] + lam[1][l2 / PB] + lam[2][o + 1]);
+          }
+          out[b1 + o * st] = a0;
+          out[b1 + (o + 1) * st] = a1;
+          if (two) {
+            out[b2 + o * st] = c0;
+            out[b2 + (o + 1) * st] = c1;
+          }
         }
-        out[q] = acc;
+      } else {
+#pragma unroll 1
+        for (int o = 0; o < PB; ++o) {
+          double a0 = 0.0, c0 = 0.0;
+#pragma unroll
+          for (int m = 0; m < PB; ++m) {
+            const double sv = Sd[m * PB + o];
+            a0 += sv * v1[m];
+            c0 += sv * v2[m];
+          }
+          if (dim == 2) {
+            a0 /= (lam[0][l % PB] + lam[1][l / PB] + lam[2][o]);
+            c0 /= (lam[0][l2 % PB] + lam[1][l2 / PB] + lam[2][o]);
+          }
+          out[b1 + o * st] = a0;
+          if (two) out[b2 + o * st] = c0;
+        }
       }
     }
     __syncthreads();
@@ -83,17 +129,39 @@ __global__ void __launch_bounds__(128) k_schwarz_local(SchwarzArgs A) {
   // backward: (Sz x Sy x Sx)
 #pragma unroll 1
   for (int dim = 0; dim < 3; ++dim) {
-    for (int l = threadIdx.x; l < PB2; l += blockDim.x) {
-      const int base = line_base(dim, l), st = STRIDE[dim];
-      double v[PB];
+    const double* Sd = S[dim];
+    for (int l = threadIdx.x; l < HALF; l += blockDim.x) {
+      const int l2 = l + HALF;
+      const bool two = l2 < PB2;
+      const int b1 = line_base(dim, l), b2 = line_base(dim, two ? l2 : l), st = STRIDE[dim];
+      double v1[PB], v2[PB];
 #pragma unroll
-      for (int m = 0; m < PB; ++m) v[m] = in[base + m * st];
-#pragma unroll 2
+      for (int m = 0; m < PB; ++m) {
+        v1[m] = in[b1 + m * st];
+        v2[m] = in[b2 + m * st];
+      }
+#pragma unroll 1
       for (int o = 0; o < PB; ++o) {
-        double acc = 0.0;
+        double a0 = 0.0, c0 = 0.0;
+        if constexpr (PAIR) {
 #pragma unroll
-        for (int m = 0; m < PB; ++m) acc += S[dim][o * PB + m] * v[m];
-        out[base + o * st] = acc;
+          for (int m = 0; m < PB; m += 2) {
+            const double2 sp = *reinterpret_cast<const double2*>(Sd + o * PB + m);
+            a0 += sp.x * v1[m];
+            a0 += sp.y * v1[m + 1];
+            c0 += sp.x * v2[m];
+            c0 += sp.y * v2[m + 1];
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < PB; ++m) {
+            const double sv = Sd[o * PB + m];
+            a0 += sv * v1[m];
+            c0 += sv * v2[m];
+          }
+        }
+        out[b1 + o * st] = a0;
+        if (two) out[b2 + o * st] = c0;
       }
     }
     __syncthreads();
@@ -104,10 +172,13 @@ __global__ void __launch_bounds__(128) k_schwarz_local(SchwarzArgs A) {
   if (A.ras) {
     for (int q = threadIdx.x; q < N1 * N1 * N1; q += blockDim.x) {
       const int i = q % N1, j = (q / N1) % N1, k = q / (N1 * N1);
-      A.Lout[e * (N1 * N1 * N1) + q] = in[(i + 1) + PB * ((j + 1) + PB * (k + 1))];
+      A.Lout[e * (N1 * N1 * N1) + q] = in[(i + 1) + PX * (j + 1) + PS * (k + 1)];
     }
   } else {
-    for (int q = threadIdx.x; q < PB3; q += blockDim.x) A.Lout[e * PB3 + q] = in[q];
+    for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
+      const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
+      A.Lout[e * PB3 + q] = in[a + PX * b + PS * c];
+    }
   }
 }
 

@@ -210,27 +210,3 @@ class PMGHierarchy:
         if getattr(self, "h", None):
             lib.cmg_pmg_destroy(self.h)
             self.h = None
-
-
-def smoke_check() -> str:
-    """One small p-MG (7,3,1) PGMRES solve on cuda:0 checked against the oracle
-    (CPU restatement driven through the reference's own templates when built)."""
-    import os
-    import sys
-
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
-    import oracle_bind as ob  # checker only
-
-    from . import chebmg as cm
-
-    desc = SemDesc(7, 3, 3, 3)
-    P = PMGHierarchy(desc, (7, 3, 1))
-    b = P.A.rhs()
-    cyc = CycleConfig(ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 4, 0)
-    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), b, None, cm.SolveOptions(tol=1e-8))
-    o = ob.OraclePmg((7, 3, 1), 3, 3, 3)
-    orep = o.solve(1, 2, 4, 0, P.A.to_canonical(b), tol=1e-8)
-    assert rep.iterations == orep.iterations, (rep.iterations, orep.iterations)
-    h, ho = np.array(rep.residual_history), np.array(orep.history)
-    assert np.max(np.abs(h - ho)) <= 1e-10 * ho[0]
-    return f"SEM p-MG(7,3,1) pgmres its={rep.iterations} mv={rep.fine_matvecs}"

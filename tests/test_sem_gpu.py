@@ -191,8 +191,14 @@ def test_determinism(cm, sem):
     assert r1.residual_history == r2.residual_history
 
 
-def test_smoke_check(sem):
-    assert "SEM" in sem.smoke_check()
+def test_graft_smoke():
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import __graft_entry__
+
+    __graft_entry__.smoke()
 
 
 @pytest.fixture(scope="module")
