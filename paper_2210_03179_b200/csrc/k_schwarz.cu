@@ -23,7 +23,7 @@ __device__ __forceinline__ int owner1d_s(int g, int ne, int& oe) {
 // line, with the 1D eigenbasis rows broadcast from shared memory (every
 // output still sums its N+3 terms in ascending order).
 template <int N>
-__global__ void __launch_bounds__(128) k_schwarz_local(SchwarzArgs A) {
+__global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, N1 = N + 1, NOS = sem_nos(N);
   // box stored with an odd x pitch: lines along x (stride PX between threads)
   // then hit distinct shared-memory banks
@@ -226,7 +226,7 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
 void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
   const long E = (long)a.Ex * a.Ey * a.Ez;
 #define X(n) \
-  if (a.N == n) { k_schwarz_local<n><<<(unsigned)E, 128, 0, s>>>(a); CMG_LAUNCH_CHECK(); return; }
+  if (a.N == n) { k_schwarz_local<n><<<(unsigned)E, 64, 0, s>>>(a); CMG_LAUNCH_CHECK(); return; }
   X(2) X(3) X(4) X(5) X(7)
 #undef X
   throw Error(EINVAL_, "Schwarz smoother: unsupported order");
