@@ -207,11 +207,24 @@ __global__ void __launch_bounds__(kRedThreads) k_cgs_mdot(const double* __restri
   for (std::size_t i = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; i < n;
        i += (std::size_t)gridDim.x * blockDim.x) {
     double v = w[i];
-    for (int l = 0; l < nv; ++l) v += -c[l] * V[(std::size_t)l * ldv + i];
-    w[i] = v;
+    if constexpr (MAXV <= 16) {  // the basis entries stay in registers for both uses
+      double vv[MAXV];
 #pragma unroll
-    for (int q = 0; q < MAXV; ++q)
-      if (q < nv) acc[q] += V[(std::size_t)q * ldv + i] * v;
+      for (int q = 0; q < MAXV; ++q) vv[q] = q < nv ? V[(std::size_t)q * ldv + i] : 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q)
+        if (q < nv) v += -c[q] * vv[q];
+      w[i] = v;
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q)
+        if (q < nv) acc[q] += vv[q] * v;
+    } else {
+      for (int l = 0; l < nv; ++l) v += -c[l] * V[(std::size_t)l * ldv + i];
+      w[i] = v;
+#pragma unroll
+      for (int q = 0; q < MAXV; ++q)
+        if (q < nv) acc[q] += V[(std::size_t)q * ldv + i] * v;
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll

@@ -2,6 +2,8 @@
 // SURVEY App. A8): overlapping (N+3)^3 extended-element subdomains solved
 // exactly by fast diagonalisation, combined additively (ASM, post-weighted)
 // or restrictively (RAS).  The definition matches oracle/oracle_schwarz.c.
+#include <cstdlib>
+
 #include "sem_kernels.hpp"
 #include "sem_layout.hpp"
 
@@ -182,6 +184,113 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   }
 }
 
+// FP64 tensor-core variant of the same local solve.  Each of the six mode
+// products is a small GEMM  out[o, line] = sum_m M(o, m) in[m, line]  with
+// M = S^T (forward) or S (backward), (N+3) x (N+3) padded to 16 x 12, and the
+// (N+3)^2 lines as the N dimension; mma.sync m8n8k4 f64 (DMMA) replaces the
+// per-line register contractions whose broadcast eigenbasis loads saturated
+// the shared-memory pipe.  4 warps per element split the 8-line column tiles.
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
+  constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, N1 = N + 1, NOS = sem_nos(N);
+  constexpr int PX = PB | 1, PS = PX * PB;
+  constexpr int MT = (PB + 7) / 8, KT = (PB + 3) / 4, NT = (PB2 + 7) / 8;
+  __shared__ double u[PS * PB], t[PS * PB];
+  __shared__ double S[3][PB2];
+  __shared__ double lam[3][PB];
+  const long e = blockIdx.x;
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  for (int d = 0; d < 3; ++d) {
+    const int id = A.sidx[e * 3 + d];
+    for (int q = threadIdx.x; q < PB2; q += blockDim.x) S[d][q] = A.S[(long)id * PB2 + q];
+    for (int q = threadIdx.x; q < PB; q += blockDim.x) lam[d][q] = A.lam[(long)id * PB + q];
+  }
+  for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
+    const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
+    int oex = 0, oey = 0, oez = 0;
+    const int ax = owner1d_s<N>(ex * N + a - 1, A.Ex, oex);
+    const int ay = owner1d_s<N>(ey * N + b - 1, A.Ey, oey);
+    const int az = owner1d_s<N>(ez * N + c - 1, A.Ez, oez);
+    double v = 0.0;
+    if (ax >= 0 && ay >= 0 && az >= 0)
+      v = A.r[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * oez)) * NOS + sem_pos(N, ax, ay, az)];
+    u[a + PX * b + PS * c] = v;
+  }
+  __syncthreads();
+  auto line_base = [](int dim, int l) {
+    const int p = l % PB, q = l / PB;
+    return dim == 0 ? PX * p + PS * q : (dim == 1 ? p + PS * q : p + PX * q);
+  };
+  constexpr int STRIDE[3] = {1, PX, PS};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tg = lane & 3;  // fragment row group / thread in group
+  double* in = u;
+  double* out = t;
+#pragma unroll 1
+  for (int pass = 0; pass < 6; ++pass) {
+    const int dim = pass % 3;
+    const bool fwd = pass < 3;
+    const int st = STRIDE[dim];
+    // A fragments (row o, col m) of M for every (m-tile, k-step)
+    double af[MT][KT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const int o = mt * 8 + g, m = kt * 4 + tg;
+        af[mt][kt] = (o < PB && m < PB) ? (fwd ? S[dim][m * PB + o] : S[dim][o * PB + m]) : 0.0;
+      }
+    for (int nt = warp; nt < NT; nt += 4) {
+      double bf[KT];
+      const int lb = nt * 8 + g;  // this thread's B column (line)
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        const int m = kt * 4 + tg;
+        bf[kt] = (lb < PB2 && m < PB) ? in[line_base(dim, lb) + m * st] : 0.0;
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) dmma_8x8x4(d0, d1, af[mt][kt], bf[kt]);
+        const int o = mt * 8 + g;
+        if (o < PB) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int l = nt * 8 + 2 * tg + i;
+            if (l < PB2) {
+              double v = i ? d1 : d0;
+              if (pass == 2) v /= (lam[0][l % PB] + lam[1][l / PB] + lam[2][o]);
+              out[line_base(dim, l) + o * st] = v;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    double* tmp = in;
+    in = out;
+    out = tmp;
+  }
+  if (A.ras) {
+    for (int q = threadIdx.x; q < N1 * N1 * N1; q += blockDim.x) {
+      const int i = q % N1, j = (q / N1) % N1, k = q / (N1 * N1);
+      A.Lout[e * (N1 * N1 * N1) + q] = in[(i + 1) + PX * (j + 1) + PS * (k + 1)];
+    }
+  } else {
+    for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
+      const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
+      A.Lout[e * PB3 + q] = in[a + PX * b + PS * c];
+    }
+  }
+}
+
 // ASM: every owned slot sums the extended local solutions covering it (fixed
 // ascending-element order, oracle_schwarz.c) and applies W = 1/count
 template <int N>
@@ -225,8 +334,21 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
 
 void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
   const long E = (long)a.Ex * a.Ey * a.Ez;
-#define X(n) \
-  if (a.N == n) { k_schwarz_local<n><<<(unsigned)E, 64, 0, s>>>(a); CMG_LAUNCH_CHECK(); return; }
+  // CUDA-core line contractions by default; the DMMA variant is opt-in
+  // (CMG_SCHWARZ_MMA=1): measured 826 vs 562 us per apply at E=32^3 -- the
+  // fragment index math and the dependent m8n8k4 chains cost more than the
+  // shared-memory traffic they remove (profiles/r01/schwarz_summary.txt)
+  static const bool use_mma = [] {
+    const char* env = std::getenv("CMG_SCHWARZ_MMA");
+    return env && std::atoi(env) == 1;
+  }();
+#define X(n)                                                                  \
+  if (a.N == n) {                                                             \
+    if (use_mma) k_schwarz_local_mma<n><<<(unsigned)E, 128, 0, s>>>(a);      \
+    else k_schwarz_local<n><<<(unsigned)E, 64, 0, s>>>(a);                    \
+    CMG_LAUNCH_CHECK();                                                       \
+    return;                                                                   \
+  }
   X(2) X(3) X(4) X(5) X(7)
 #undef X
   throw Error(EINVAL_, "Schwarz smoother: unsupported order");

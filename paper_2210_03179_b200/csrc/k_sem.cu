@@ -842,12 +842,25 @@ __global__ void __launch_bounds__(256) k_layer_cgs_dots(const double* __restrict
   for (long q = (long)chunk * blockDim.x + threadIdx.x; q < layer_len; q += (long)LCH * blockDim.x) {
     const std::size_t i = base + q;
     double v = w[i];
-    // unfused multiply-add, as k_cgs_update (k_blas.cu is built with --fmad=false)
-    for (int l = 0; l < nv; ++l) v = __dadd_rn(v, __dmul_rn(-c[l], V[(std::size_t)l * ldv + i]));
-    w[i] = v;
+    if constexpr (MAXV <= 16) {  // the basis entries stay in registers for both uses
+      double vv[MAXV];
 #pragma unroll
-    for (int l = 0; l < MAXV; ++l)
-      if (l < nv) acc[l] += V[(std::size_t)l * ldv + i] * v;
+      for (int l = 0; l < MAXV; ++l) vv[l] = l < nv ? V[(std::size_t)l * ldv + i] : 0.0;
+      // unfused multiply-add, as k_cgs_update (k_blas.cu is built with --fmad=false)
+#pragma unroll
+      for (int l = 0; l < MAXV; ++l)
+        if (l < nv) v = __dadd_rn(v, __dmul_rn(-c[l], vv[l]));
+      w[i] = v;
+#pragma unroll
+      for (int l = 0; l < MAXV; ++l)
+        if (l < nv) acc[l] += vv[l] * v;
+    } else {
+      for (int l = 0; l < nv; ++l) v = __dadd_rn(v, __dmul_rn(-c[l], V[(std::size_t)l * ldv + i]));
+      w[i] = v;
+#pragma unroll
+      for (int l = 0; l < MAXV; ++l)
+        if (l < nv) acc[l] += V[(std::size_t)l * ldv + i] * v;
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
