@@ -295,7 +295,7 @@ def main():
     peak, peak_src = peaks()
     achieved = per_gpu_bytes / step_s / 1e9
     # measured DRAM traffic of the same pair: ncu --set full at E=64^3 (profiles/r01/sem_step_E64_summary.txt),
-    # K1 10.664 GB + K2 2.527 GB per step, scaled per element to this run's slab
+    # K1 10.665 GB + K2 2.522 GB per step, scaled per element to this run's slab
     traffic = (10.665e9 + 2.522e9) / 64 ** 3 * (E ** 3 / world)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": "ncu dram__bytes_read+write, K1+K2 per step, profiles/r01",
