@@ -303,28 +303,30 @@ def main():
             "algorithmic_bytes_per_step": per_gpu_bytes, "peak_source": peak_src}
 
     # e2e through the public API with host buffers: every step copies its b, x
-    # in from pinned host memory, sweeps, and copies x out.  Double-buffered:
+    # in from pinned host memory, sweeps, and copies x out.  Triple-buffered:
     # step i+1's inputs stream in (copy stream) while step i computes and step
-    # i-1's result streams out (second copy stream), as a solver service would.
+    # i-1's result streams out (second copy stream), as a solver service would;
+    # a buffer is refilled only after its previous result has been copied out.
+    NB = 3
     hb = b.detach().cpu().pin_memory()
     hx = x.detach().cpu().pin_memory()
     hout = torch.empty_like(hx).pin_memory()
-    bufs = [(b, x), (torch.empty_like(b), torch.empty_like(x))]
+    bufs = [(b, x)] + [(torch.empty_like(b), torch.empty_like(x)) for _ in range(NB - 1)]
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_free = [torch.cuda.Event() for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(NB)]
+    ev_done = [torch.cuda.Event() for _ in range(NB)]
+    ev_free = [torch.cuda.Event() for _ in range(NB)]
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(2, min(args.steps, 6))
+    e2e_steps = max(NB, min(args.steps, 8))
     e0.record(stream)
     s_in.wait_event(e0)
     for i in range(e2e_steps):
-        k = i % 2
+        k = i % NB
         bb, xx = bufs[k]
         with torch.cuda.stream(s_in):
-            if i >= 2:
-                s_in.wait_event(ev_free[k])  # the D2H of step i-2 has read this x
+            if i >= NB:
+                s_in.wait_event(ev_free[k])  # the D2H of step i-NB has read this x
             bb.copy_(hb, non_blocking=True)
             xx.copy_(hx, non_blocking=True)
             ev_in[k].record(s_in)
@@ -335,7 +337,7 @@ def main():
             s_out.wait_event(ev_done[k])
             hout.copy_(xx, non_blocking=True)
             ev_free[k].record(s_out)
-    stream.wait_event(ev_free[(e2e_steps - 1) % 2])
+    stream.wait_event(ev_free[(e2e_steps - 1) % NB])
     e1.record(stream)
     barrier()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
