@@ -279,6 +279,13 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
     }
   }
   const double* Ge = A.G + e * 6 * NP;
+  if (A.prefetch_g) {
+    // pull the element's factors toward L2 now: the geometry phase's register
+    // loads then wait on L2 instead of HBM while gather/gradient run
+    constexpr int LINES = 6 * NP * 8 / 128;
+    for (int q = t; q < LINES; q += (N + 1) * (N + 1) * KS)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(Ge + q * 16));
+  }
   double wt[KH], dvh[KH];
   ON_PART(gather, A, su, ta, tb, e);
   __syncthreads();

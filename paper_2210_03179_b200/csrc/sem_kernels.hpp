@@ -68,6 +68,7 @@ struct SemArgs {
   // K2 needs whole element layers)
   long e_begin = 0, e_end = 0;
   int k2_z0 = 0;  // first local layer of a K2 launch (set by the launcher)
+  int prefetch_g = 0;  // K1: L2 prefetch of the element's geometric factors at block start
 };
 
 // upload the order-N GLL derivative matrix to constant memory (once per order)
