@@ -324,16 +324,15 @@ __global__ void k_sem_k1_lvec(SemArgs A) {
 constexpr int k2_eb(int N) { return sem_nshared(N) >= 256 ? 1 : 256 / sem_nshared(N); }
 
 // One owned shared node: sum its <= 8 shell contributions in the fixed
-// (dz, dy, dx) order, then the step's epilogue.  CG: read the shell through L2
-// only (for a caller that reads contributions written in the same launch).
-// Returns without work for padding slots.
+// (dz, dy, dx) order, then the step's epilogue.  Returns without work for
+// padding slots.
 //
 // A single-launch step that ran this per owned node inside the element kernel
 // (elements claimed in decreasing order, per-element "shell written" flags)
 // was measured at E=64^3: 21.9 vs 34.1 GDOF-step/s for the K1 + K2 pair --
 // waiting for the +x neighbour's flag cost 1.15 ms and the in-block node work
 // 0.7 ms per step, against 0.47 ms for the separate K2 launch.
-template <int N, int EPI, bool CG>
+template <int N, int EPI>
 __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey, int ez, int s) {
   constexpr int N1 = N + 1, NOS = sem_nos(N), NINT = sem_nint(N);
   // host-built table (sem.cpp, L1-resident): [count, a|b<<8|c<<16, (offset, dx|dy<<1|dz<<2) x count],
@@ -357,7 +356,7 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
         const int i2 = (a + 1) - dx * N, j2 = (b + 1) - dy * N;
         vals[cidx] = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + i2 + N1 * j2];
       } else {
-        vals[cidx] = CG ? __ldcg(sh + off) : sh[off];
+        vals[cidx] = sh[off];
       }
     }
   }
@@ -389,7 +388,7 @@ __global__ void k_sem_k2(SemArgs A) {
   const int ex = blockIdx.x * k2_eb(N) + q, ey = blockIdx.y, ez = blockIdx.z + A.k2_z0;
   if (q >= k2_eb(N) || ex >= A.Ex) return;
   const long e = ex + (long)A.Ex * (ey + (long)A.Ey * ez);
-  k2_node<N, EPI, false>(A, e, ex, ey, ez, s);
+  k2_node<N, EPI>(A, e, ex, ey, ez, s);
 }
 
 template <int N, int MODE, int EPI>
