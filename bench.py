@@ -201,6 +201,47 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- BASELINE configs[1..3]
+def baseline_config_solves(cm, sem, ctx, stream):
+    """Full-size solves of the other BASELINE configs on this GPU (p-MG(7,3,1)
+    PGMRES(30), tol 1e-8): iterations, fine matvecs and device time to
+    solution, each after a warm-up solve.  tools/config_table.py has the full grid."""
+    import torch
+
+    def solve(P, fam, kpre, kpost):
+        cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
+        M = P.preconditioner(cyc)
+        b = P.A.rhs()
+        opts = cm.SolveOptions(tol=1e-8, restart=30, maxit=500)
+        cm.pgmres(P.A, M, b, None, opts)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, rep = cm.pgmres(P.A, M, b, None, opts)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return {"cycle": f"({kpre},{kpost})", "family": cm.Family(fam).name, "iterations": rep.iterations,
+                "fine_matvecs": rep.fine_matvecs, "converged": rep.converged,
+                "time_to_solution_ms": e0.elapsed_time(e1)}
+
+    out = {}
+    P = sem.PMGHierarchy(sem.SemDesc(7, 16, 16, 16), (7, 3, 1), ctx=ctx)
+    out["configs[1] box N=7 E=16^3, Chebyshev-Jacobi"] = [solve(P, f, kp, kq) for f in (0, 2, 3)
+                                                          for kp, kq in ((8, 0), (4, 4))]
+    del P
+    rows = []
+    for smoother, name in ((sem.RAS, "RAS"), (sem.ASM, "ASM")):
+        P = sem.PMGHierarchy(sem.SemDesc(7, 32, 32, 32), (7, 3, 1), smoother=smoother, ctx=ctx)
+        rows += [dict(solve(P, 2, kp, kq), smoother=name) for kp, kq in ((2, 0), (1, 1))]
+        del P
+    out["configs[2] box N=7 E=32^3, Chebyshev-Schwarz (FDM local solves)"] = rows
+    P = sem.PMGHierarchy(sem.SemDesc(7, 32, 32, 32, geometry=sem.KERSHAW, eps=0.3), (7, 3, 1), ctx=ctx)
+    out["configs[3] Kershaw eps=0.3 N=7 E=32^3, Chebyshev-Jacobi"] = [solve(P, 2, kp, kq)
+                                                                     for kp, kq in ((8, 0), (4, 4))]
+    del P
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -213,6 +254,7 @@ def main():
     ap.add_argument("--cpu-E", dest="cpu_E", type=int, default=12)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs[1..3] solves")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -374,6 +416,7 @@ def main():
 
     fd = None
     cpu = None
+    configs = None
     if rank == 0 and world == 1:
         # FD config 1: n=256 (255^2 unknowns), PGMRES + 4th-kind (4,0) half V-cycle, factor 2, Lx=1
         h = cm.build_hierarchy(cm.Domain(1.0, 1.0, 256), 2, ctx=ctx)
@@ -425,6 +468,8 @@ def main():
                          "note": "peak is the measured copy (1 read : 1 write) bandwidth; this stream is 4 reads "
                                  ": 3 writes and can exceed it"}}
         del Af, invf, bf, xf
+        if not args.no_configs:
+            configs = baseline_config_solves(cm, sem, ctx, stream)
         if not args.no_cpu:
             v, kind, sample = cpu_reference_sweep(args.cpu_E, order, reps=50, seconds_cap=15.0)
             cpu = {"value": v, "unit": "GDOF-step/s", "cores": 1, "kind": kind, "sample": sample}
@@ -442,7 +487,7 @@ def main():
                                                             f"{A.vec_len() * 8 / 1e6:.0f} MB/GPU, G "
                                                             f"{6 * 512 * E ** 3 * 8 / world / 1e9:.1f} GB/GPU)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "time_to_solution": tts, "fd_config1": fd,
+            "clocks": clk.summary(), "time_to_solution": tts, "fd_config1": fd, "baseline_configs": configs,
             "setup_s": t_setup, "step_ms_min_max": [min(step_ms), max(step_ms)],
         }
         print(json.dumps(line), flush=True)
