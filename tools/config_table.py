@@ -71,6 +71,14 @@ def main():
                     run(f"configs[3] Kershaw eps={eps} E=32^3 Jacobi", P, fam, k, k)
                     run(f"configs[3] Kershaw eps={eps} E=32^3 Jacobi", P, fam, 2 * k, 0)
             del P
+    if "paper" in only:
+        # PAPER.md tab:ksp-comparison: Kershaw E=47K (36^3), p=7, 1st-kind Chebyshev-Jacobi (3,3),
+        # (7,5,3,1) p-MG, PGMRES(30), tol 1e-8 -> 9 / 123 / 474 iterations at eps = 1 / 0.3 / 0.05
+        # (the paper's coarsest level is one AMG V-cycle; here an exact p=1 solve)
+        for eps, paper_its in ((1.0, 9), (0.3, 123), (0.05, 474)):
+            P = sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 36, geometry=sem.KERSHAW, eps=eps), (7, 5, 3, 1), ctx=ctx)
+            run(f"paper Kershaw eps={eps} E=36^3 (7,5,3,1) [paper PGMRES: {paper_its} its]", P, 0, 3, 3)
+            del P
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as fh:
         json.dump({"device": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%d %H:%M:%S"),
