@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <cusolverDn.h>
+
 #include "cmg_objects.hpp"
 #include "sem_kernels.hpp"
 #include "sem_layout.hpp"
@@ -508,6 +510,15 @@ struct cmg_pmg {
   };
   std::vector<std::unique_ptr<Schwarz>> sch;
   int cnx = 0, cny = 0, cnz = 0;
+  // dense Cholesky factor of the deformed-mesh p=1 operator (k_sem_coarse.cu)
+  cusolverDnHandle_t sol = nullptr;
+  DBuf cA, cwork, cb;
+  int* cinfo = nullptr;
+  int cn = 0;
+  ~cmg_pmg() {
+    if (sol) cusolverDnDestroy(sol);
+    if (cinfo) cudaFree(cinfo);
+  }
 };
 
 namespace {
@@ -563,6 +574,59 @@ void pmg_fdm_box(cmg_pmg* p, const double* rc, double* ec) {
   }
 }
 
+// Deformed mesh: assemble the p=1 operator from 27 colour probes (k_sem_coarse.cu)
+// into a dense matrix and Cholesky-factor it once (cuSOLVER), when it has at
+// most CMG_COARSE_DENSE_MAX (default 46340, i.e. < 2^31 entries) unknowns;
+// larger coarse problems keep the CG below.  Partitioned: every rank gathers
+// all rows and factors redundantly (the coarse solve is replicated anyway).
+void coarse_dense_setup(cmg_pmg* p) {
+  SemLevel* C = p->lev.back().get();
+  const long n = static_cast<long>(p->cnx) * p->cny * p->cnz;
+  long cap = 46340;
+  if (const char* env = std::getenv("CMG_COARSE_DENSE_MAX")) cap = std::min(cap, std::atol(env));
+  if (n < 1 || n > cap) return;
+  cudaStream_t s = p->ctx->stream;
+  const CoarseGrid g{C->Ex, C->Ey, C->Ezl, C->z0, p->cnx, p->cny, p->cnz};
+  const long rows_local = static_cast<long>(p->cnx) * p->cny * C->Ezl;
+  DBuf v(C->len), y(C->len), rl(rows_local * 27), rg;
+  rl.zero(s);
+  const std::size_t cnt0 = C->count;
+  for (int cz = 0; cz < 3; ++cz)
+    for (int cy = 0; cy < 3; ++cy)
+      for (int cx = 0; cx < 3; ++cx) {
+        coarse_probe(g, cx, cy, cz, v.p, s);
+        C->apply(v.p, y.p);
+        coarse_probe_extract(g, cx, cy, cz, y.p, rl.p, s);
+      }
+  C->count = cnt0;
+  const double* rows = rl.p;
+  if (C->distributed()) {
+    rg.alloc(static_cast<std::size_t>(rows_local) * 27 * C->desc.nranks);
+    p->ctx->comm->allgather(rl.p, rg.p, static_cast<std::size_t>(rows_local) * 27, s);
+    rows = rg.p;
+  }
+  p->cA.alloc(static_cast<std::size_t>(n) * n);
+  p->cA.zero(s);
+  coarse_dense_build(g, rows, p->cA.p, s);
+  if (cusolverDnCreate(&p->sol) != CUSOLVER_STATUS_SUCCESS) fail(CMG_ERUNTIME, "pmg: cusolverDnCreate failed");
+  cusolverDnSetStream(p->sol, s);
+  int lwork = 0;
+  if (cusolverDnDpotrf_bufferSize(p->sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), p->cA.p, static_cast<int>(n),
+                                  &lwork) != CUSOLVER_STATUS_SUCCESS)
+    fail(CMG_ERUNTIME, "pmg: potrf buffer size failed");
+  p->cwork.alloc(std::max(lwork, 1));
+  CMG_CUDA(cudaMalloc(&p->cinfo, sizeof(int)));
+  if (cusolverDnDpotrf(p->sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), p->cA.p, static_cast<int>(n), p->cwork.p,
+                       lwork, p->cinfo) != CUSOLVER_STATUS_SUCCESS)
+    fail(CMG_ERUNTIME, "pmg: coarse potrf failed");
+  int info = 0;
+  CMG_CUDA(cudaMemcpyAsync(&info, p->cinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CMG_CUDA(cudaStreamSynchronize(s));
+  if (info != 0) fail(CMG_ERUNTIME, "pmg: coarse p=1 operator not positive definite");
+  p->cb.alloc(n);
+  p->cn = static_cast<int>(n);
+}
+
 // p=1 solve.  Box: the FDM solve is exact.  Deformed (Kershaw) mesh: the
 // rediscretised p=1 operator is not separable, so the coarse solve is CG on
 // A_1 preconditioned by the box FDM, run to a relative residual of 1e-13
@@ -572,6 +636,21 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
   SemLevel* c = p->lev.back().get();
   if (c->desc.geometry == 0) {
     pmg_fdm_box(p, rc, ec);
+    return;
+  }
+  if (p->cn > 0) {  // dense Cholesky solve (coarse_dense_setup)
+    cudaStream_t s = p->ctx->stream;
+    const double* in = rc;
+    if (c->distributed()) {
+      p->ctx->comm->allgather(rc, p->cfull.p, c->len, s);
+      in = p->cfull.p;
+    }
+    const CoarseGrid g{c->Ex, c->Ey, c->Ezl, c->z0, p->cnx, p->cny, p->cnz};
+    coarse_slots_to_dense(g, in, p->cb.p, s);
+    if (cusolverDnDpotrs(p->sol, CUBLAS_FILL_MODE_LOWER, p->cn, 1, p->cA.p, p->cn, p->cb.p, p->cn, p->cinfo) !=
+        CUSOLVER_STATUS_SUCCESS)
+      fail(CMG_ERUNTIME, "pmg: coarse potrs failed");
+    coarse_dense_to_slots(g, p->cb.p, ec, s);
     return;
   }
   cmg_ctx* ctx = p->ctx;
@@ -915,6 +994,7 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
       b->alloc(C->len);
       b->zero(s);
     }
+    if (C->desc.geometry != 0) coarse_dense_setup(p.get());
     // lambda_tilde per smoothed level (smoothers.hpp:61-79; S = invD or the Schwarz operator)
     p->lambda.assign(nlevels, 0.0);
     for (int l = 0; l + 1 < nlevels; ++l) {

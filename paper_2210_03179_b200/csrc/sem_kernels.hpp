@@ -125,6 +125,21 @@ void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* 
 void sem_layer_finalize(const double* gathered, int nv, const int* layers_per_rank, int nranks,
                         double* out, int do_sqrt, cudaStream_t s);
 
+// dense direct p=1 coarse solve (deformed meshes), k_sem_coarse.cu
+struct CoarseGrid {
+  int Ex, Ey, Ezl, z0;  // p=1 element grid of this rank's slab
+  int nx, ny, nz;       // global interior vertices per direction (unknowns nx*ny*nz)
+};
+// colour probe vector (vertices with (ix%3, iy%3, iz%3) == (cx, cy, cz)) in slot layout
+void coarse_probe(const CoarseGrid& g, int cx, int cy, int cz, double* v, cudaStream_t s);
+// rows[local row][27] entries A(i, i+o) read off the probe's image y
+void coarse_probe_extract(const CoarseGrid& g, int cx, int cy, int cz, const double* y, double* rows,
+                          cudaStream_t s);
+// dense column-major A from the gathered rows (A zeroed by the caller)
+void coarse_dense_build(const CoarseGrid& g, const double* rows, double* A, cudaStream_t s);
+void coarse_slots_to_dense(const CoarseGrid& g, const double* full, double* b, cudaStream_t s);
+void coarse_dense_to_slots(const CoarseGrid& g, const double* x, double* ec, cudaStream_t s);
+
 // Schwarz (ASM/RAS) with FDM local solves
 // single-rank (the Schwarz configs are 1-GPU, BASELINE configs[2])
 struct SchwarzArgs {
