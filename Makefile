@@ -42,7 +42,7 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(HDR)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static $(NCCL_LINK) -L$(CUDA)/lib64 -lcusolver -Xlinker -rpath=$(CUDA)/lib64 -lpthread -ldl -lrt -Xlinker --no-undefined
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static $(NCCL_LINK) -L$(CUDA)/lib64 -lcusolver -lcublas -Xlinker -rpath=$(CUDA)/lib64 -lpthread -ldl -lrt -Xlinker --no-undefined
 
 oracle:
 	$(MAKE) -C oracle

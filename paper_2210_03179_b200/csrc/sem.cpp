@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include "cmg_objects.hpp"
@@ -512,11 +513,13 @@ struct cmg_pmg {
   int cnx = 0, cny = 0, cnz = 0;
   // dense Cholesky factor of the deformed-mesh p=1 operator (k_sem_coarse.cu)
   cusolverDnHandle_t sol = nullptr;
-  DBuf cA, cwork, cb;
+  cublasHandle_t blas = nullptr;  // set when the explicit inverse is used
+  DBuf cA, cwork, cb, cx;
   int* cinfo = nullptr;
   int cn = 0;
   ~cmg_pmg() {
     if (sol) cusolverDnDestroy(sol);
+    if (blas) cublasDestroy(blas);
     if (cinfo) cudaFree(cinfo);
   }
 };
@@ -625,6 +628,27 @@ void coarse_dense_setup(cmg_pmg* p) {
   if (info != 0) fail(CMG_ERUNTIME, "pmg: coarse p=1 operator not positive definite");
   p->cb.alloc(n);
   p->cn = static_cast<int>(n);
+  // Default: form the inverse from the factor once (potri) and apply it as one
+  // symmetric matrix-vector product per coarse solve -- a single bandwidth-bound
+  // pass over the lower triangle instead of two latency-bound triangular
+  // solves.  CMG_COARSE_INV=0 keeps potrs.
+  const char* inv_env = std::getenv("CMG_COARSE_INV");
+  if (inv_env && std::atoi(inv_env) == 0) return;
+  int lw2 = 0;
+  if (cusolverDnDpotri_bufferSize(p->sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), p->cA.p, static_cast<int>(n),
+                                  &lw2) != CUSOLVER_STATUS_SUCCESS)
+    fail(CMG_ERUNTIME, "pmg: potri buffer size failed");
+  if (static_cast<std::size_t>(lw2) > p->cwork.n) p->cwork.alloc(lw2);
+  if (cusolverDnDpotri(p->sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), p->cA.p, static_cast<int>(n), p->cwork.p,
+                       lw2, p->cinfo) != CUSOLVER_STATUS_SUCCESS)
+    fail(CMG_ERUNTIME, "pmg: coarse potri failed");
+  CMG_CUDA(cudaMemcpyAsync(&info, p->cinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CMG_CUDA(cudaStreamSynchronize(s));
+  if (info != 0) fail(CMG_ERUNTIME, "pmg: coarse inverse failed");
+  if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) fail(CMG_ERUNTIME, "pmg: cublasCreate failed");
+  cublasSetStream(p->blas, s);
+  cublasSetPointerMode(p->blas, CUBLAS_POINTER_MODE_HOST);
+  p->cx.alloc(n);
 }
 
 // p=1 solve.  Box: the FDM solve is exact.  Deformed (Kershaw) mesh: the
@@ -647,6 +671,14 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
     }
     const CoarseGrid g{c->Ex, c->Ey, c->Ezl, c->z0, p->cnx, p->cny, p->cnz};
     coarse_slots_to_dense(g, in, p->cb.p, s);
+    if (p->blas) {  // x = A^{-1} b with the symmetric inverse's lower triangle (one HBM pass)
+      const double one = 1.0, zero = 0.0;
+      if (cublasDsymv(p->blas, CUBLAS_FILL_MODE_LOWER, p->cn, &one, p->cA.p, p->cn, p->cb.p, 1, &zero, p->cx.p, 1) !=
+          CUBLAS_STATUS_SUCCESS)
+        fail(CMG_ERUNTIME, "pmg: coarse symv failed");
+      coarse_dense_to_slots(g, p->cx.p, ec, s);
+      return;
+    }
     if (cusolverDnDpotrs(p->sol, CUBLAS_FILL_MODE_LOWER, p->cn, 1, p->cA.p, p->cn, p->cb.p, p->cn, p->cinfo) !=
         CUSOLVER_STATUS_SUCCESS)
       fail(CMG_ERUNTIME, "pmg: coarse potrs failed");
