@@ -695,96 +695,131 @@ __global__ void k_slot_mask(SemArgs A, double* __restrict__ m) {
 }
 
 // ---------------------------------------------------------------- p-transfers
-// one block per fine element; smem staging of the coarse element values
+// tepb(NF) elements per 128-thread block (smem staging per element): for the
+// small low-order elements each thread then keeps several independent loads in
+// flight (prolong/restrict 3->1: 130/108 vs 220/212 us at E=64^3); the order-7
+// elements already fill the threads and keep one element per block (more
+// blocks per SM: 704/568 vs 857/775 us with four).
+constexpr int tepb(int NF) { return NF >= 5 ? 1 : 4; }
+
 template <int NF, int NCO>
-__global__ void k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
-                          const double* __restrict__ xc, double* __restrict__ yf, int add) {
+__global__ void __launch_bounds__(128) k_prolong(SemArgs F, SemArgs Cc, const double* __restrict__ J,
+                                                 const double* __restrict__ xc, double* __restrict__ yf, int add) {
+  constexpr int TEPB = tepb(NF);
   constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF;
   constexpr int NOSF = sem_nos(NF), NOSC = sem_nos(NCO);
+  constexpr int UC = C1 * C1 * C1, T1 = F1 * C1 * C1, T2 = F1 * F1 * C1;
   __shared__ double sJ[F1 * C1];
-  __shared__ double uc[C1 * C1 * C1];
-  __shared__ double t1[F1 * C1 * C1];
-  __shared__ double t2[F1 * F1 * C1];
-  const long e = blockIdx.x;
-  const int ex = (int)(e % F.Ex), ey = (int)((e / F.Ex) % F.Ey), ez = (int)(e / ((long)F.Ex * F.Ey));
+  __shared__ double uc[TEPB][UC];
+  __shared__ double t1[TEPB][T1];
+  __shared__ double t2[TEPB][T2];
+  __shared__ int sxyz[TEPB][3];  // element coordinates (the divisions done once per element)
+  const long e0 = (long)blockIdx.x * TEPB, E = F.e_end;
   for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
-  for (int q = threadIdx.x; q < C1 * C1 * C1; q += blockDim.x) {
-    const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
-    int oex = 0, oey = 0, oez = 0;
-    const int ax = owner1d<NCO>(ex, a, Cc.Ex, oex);
-    const int ay = owner1d<NCO>(ey, b, Cc.Ey, oey);
-    const int az = owner1d<NCO>(Cc.z0 + ez, c, Cc.Ez, oez);
-    double v = 0.0;
-    if (ax >= 0 && ay >= 0 && az >= 0) {
-      const int lz = oez - Cc.z0;
-      if (lz < 0)
-        v = Cc.halo_lo[((long)oex + (long)Cc.Ex * oey) * (NCO * NCO) + ax + NCO * ay];
-      else
-        v = xc[((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOSC + sem_pos(NCO, ax, ay, az)];
-    }
-    uc[q] = v;
+  if (threadIdx.x < TEPB) {
+    const long e = e0 + threadIdx.x;
+    sxyz[threadIdx.x][0] = (int)(e % F.Ex);
+    sxyz[threadIdx.x][1] = (int)((e / F.Ex) % F.Ey);
+    sxyz[threadIdx.x][2] = (int)(e / ((long)F.Ex * F.Ey));
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < F1 * C1 * C1; q += blockDim.x) {  // contract x
+  for (int qq = threadIdx.x; qq < TEPB * UC; qq += blockDim.x) {
+    const int le = qq / UC, q = qq - le * UC;
+    const long e = e0 + le;
+    double v = 0.0;
+    if (e < E) {
+      const int ex = sxyz[le][0], ey = sxyz[le][1], ez = sxyz[le][2];
+      const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
+      int oex = 0, oey = 0, oez = 0;
+      const int ax = owner1d<NCO>(ex, a, Cc.Ex, oex);
+      const int ay = owner1d<NCO>(ey, b, Cc.Ey, oey);
+      const int az = owner1d<NCO>(Cc.z0 + ez, c, Cc.Ez, oez);
+      if (ax >= 0 && ay >= 0 && az >= 0) {
+        const int lz = oez - Cc.z0;
+        if (lz < 0)
+          v = Cc.halo_lo[((long)oex + (long)Cc.Ex * oey) * (NCO * NCO) + ax + NCO * ay];
+        else
+          v = xc[((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOSC + sem_pos(NCO, ax, ay, az)];
+      }
+    }
+    uc[le][q] = v;
+  }
+  __syncthreads();
+  for (int qq = threadIdx.x; qq < TEPB * T1; qq += blockDim.x) {  // contract x
+    const int le = qq / T1, q = qq - le * T1;
     const int i = q % F1, b = (q / F1) % C1, c = q / (F1 * C1);
     double v = 0.0;
-    for (int m = 0; m < C1; ++m) v += sJ[i * C1 + m] * uc[m + C1 * (b + C1 * c)];
-    t1[q] = v;
+    for (int m = 0; m < C1; ++m) v += sJ[i * C1 + m] * uc[le][m + C1 * (b + C1 * c)];
+    t1[le][q] = v;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < F1 * F1 * C1; q += blockDim.x) {  // contract y
+  for (int qq = threadIdx.x; qq < TEPB * T2; qq += blockDim.x) {  // contract y
+    const int le = qq / T2, q = qq - le * T2;
     const int i = q % F1, j = (q / F1) % F1, c = q / (F1 * F1);
     double v = 0.0;
-    for (int m = 0; m < C1; ++m) v += sJ[j * C1 + m] * t1[i + F1 * (m + C1 * c)];
-    t2[q] = v;
+    for (int m = 0; m < C1; ++m) v += sJ[j * C1 + m] * t1[le][i + F1 * (m + C1 * c)];
+    t2[le][q] = v;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < NOF; q += blockDim.x) {  // contract z at owned fine nodes
+  for (int qq = threadIdx.x; qq < TEPB * NOF; qq += blockDim.x) {  // contract z at owned fine nodes
+    const int le = qq / NOF, q = qq - le * NOF;
+    const long e = e0 + le;
+    if (e >= E) continue;
+    const int ex = sxyz[le][0], ey = sxyz[le][1], ez = sxyz[le][2];
     const int a = q % NF, b = (q / NF) % NF, c = q / (NF * NF);
     const int i = a + 1, j = b + 1, k = c + 1;
     if (ex * NF + i >= NF * F.Ex || ey * NF + j >= NF * F.Ey || (F.z0 + ez) * NF + k >= NF * F.Ez) continue;
     double v = 0.0;
-    for (int m = 0; m < C1; ++m) v += sJ[k * C1 + m] * t2[i + F1 * (j + F1 * m)];
+    for (int m = 0; m < C1; ++m) v += sJ[k * C1 + m] * t2[le][i + F1 * (j + F1 * m)];
     const long slot = e * NOSF + sem_pos(NF, a, b, c);
     yf[slot] = add ? yf[slot] + v : v;
   }
 }
 
 template <int NF, int NCO>
-__global__ void k_restrict_local(SemArgs F, const double* __restrict__ J, const double* __restrict__ xf,
-                                 double* __restrict__ Lc) {
+__global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double* __restrict__ J,
+                                                        const double* __restrict__ xf, double* __restrict__ Lc) {
+  constexpr int TEPB = tepb(NF);
   constexpr int F1 = NF + 1, C1 = NCO + 1, CP = C1 * C1 * C1, NOSF = sem_nos(NF);
+  constexpr int UF = F1 * F1 * F1, T1 = C1 * F1 * F1, T2 = C1 * C1 * F1;
   __shared__ double sJ[F1 * C1];
-  __shared__ double uf[F1 * F1 * F1];
-  __shared__ double t1[C1 * F1 * F1];
-  __shared__ double t2[C1 * C1 * F1];
-  const long e = blockIdx.x;
+  __shared__ double uf[TEPB][UF];
+  __shared__ double t1[TEPB][T1];
+  __shared__ double t2[TEPB][T2];
+  const long e0 = (long)blockIdx.x * TEPB, E = F.e_end;
   for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
-  for (int q = threadIdx.x; q < F1 * F1 * F1; q += blockDim.x) {
+  for (int qq = threadIdx.x; qq < TEPB * UF; qq += blockDim.x) {
+    const int le = qq / UF, q = qq - le * UF;
+    const long e = e0 + le;
     const int i = q % F1, j = (q / F1) % F1, k = q / (F1 * F1);
     double v = 0.0;
-    if (i >= 1 && j >= 1 && k >= 1) v = xf[e * NOSF + sem_pos(NF, i - 1, j - 1, k - 1)];
-    uf[q] = v;  // padding slots are zero
+    if (e < E && i >= 1 && j >= 1 && k >= 1) v = xf[e * NOSF + sem_pos(NF, i - 1, j - 1, k - 1)];
+    uf[le][q] = v;  // padding slots are zero
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < C1 * F1 * F1; q += blockDim.x) {  // J^T along x
+  for (int qq = threadIdx.x; qq < TEPB * T1; qq += blockDim.x) {  // J^T along x
+    const int le = qq / T1, q = qq - le * T1;
     const int a = q % C1, j = (q / C1) % F1, k = q / (C1 * F1);
     double v = 0.0;
-    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + a] * uf[m + F1 * (j + F1 * k)];
-    t1[q] = v;
+    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + a] * uf[le][m + F1 * (j + F1 * k)];
+    t1[le][q] = v;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < C1 * C1 * F1; q += blockDim.x) {
+  for (int qq = threadIdx.x; qq < TEPB * T2; qq += blockDim.x) {
+    const int le = qq / T2, q = qq - le * T2;
     const int a = q % C1, b = (q / C1) % C1, k = q / (C1 * C1);
     double v = 0.0;
-    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + b] * t1[a + C1 * (m + F1 * k)];
-    t2[q] = v;
+    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + b] * t1[le][a + C1 * (m + F1 * k)];
+    t2[le][q] = v;
   }
   __syncthreads();
-  for (int q = threadIdx.x; q < CP; q += blockDim.x) {
+  for (int qq = threadIdx.x; qq < TEPB * CP; qq += blockDim.x) {
+    const int le = qq / CP, q = qq - le * CP;
+    const long e = e0 + le;
+    if (e >= E) continue;
     const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
     double v = 0.0;
-    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + c] * t2[a + C1 * (b + C1 * m)];
+    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + c] * t2[le][a + C1 * (b + C1 * m)];
     Lc[e * CP + q] = v;
   }
 }
@@ -991,13 +1026,17 @@ void sem_slot_mask(const SemArgs& a, double* mask, cudaStream_t s) {
 template <int NF, int NCO>
 static void prolong_t(const SemArgs& f, const SemArgs& c, const double* J, const double* xc, double* yf,
                       bool add, cudaStream_t s) {
-  k_prolong<NF, NCO><<<(unsigned)f.E, 128, 0, s>>>(f, c, J, xc, yf, add ? 1 : 0);
+  SemArgs ff = f;
+  ff.e_end = f.E;
+  k_prolong<NF, NCO><<<(unsigned)((f.E + tepb(NF) - 1) / tepb(NF)), 128, 0, s>>>(ff, c, J, xc, yf, add ? 1 : 0);
   CMG_LAUNCH_CHECK();
 }
 
 template <int NF, int NCO>
 static void restrict_t(const SemArgs& f, const double* J, const double* xf, double* Lc, cudaStream_t s) {
-  k_restrict_local<NF, NCO><<<(unsigned)f.E, 128, 0, s>>>(f, J, xf, Lc);
+  SemArgs ff = f;
+  ff.e_end = f.E;
+  k_restrict_local<NF, NCO><<<(unsigned)((f.E + tepb(NF) - 1) / tepb(NF)), 128, 0, s>>>(ff, J, xf, Lc);
   CMG_LAUNCH_CHECK();
 }
 
