@@ -1,0 +1,32 @@
+"""The runtime A/B knobs select alternative kernels; every
+non-default variant must pass the same parity checks as the default.  Each
+knob is read once per process, so each variant runs the relevant parity tests
+in a child pytest with the variable set."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+VARIANTS = [
+    ("CMG_K1_GREG", "0", "tests/test_sem_gpu.py", "apply_diag_rhs or sweeps_all_families or pmg_solves"),
+    ("CMG_K1_PREFETCH", "0", "tests/test_sem_gpu.py", "sweeps_all_families"),
+    ("CMG_SHELL_LEX", "1", "tests/test_sem_gpu.py", "apply_diag_rhs or sweeps_all_families or v_cycle"),
+    ("CMG_CGS_FUSE", "0", "tests/test_sem_gpu.py", "pmg_solves"),
+    ("CMG_CGS_FUSE", "0", "tests/test_fd_gpu.py", "golden_solves"),
+    ("CMG_FD_GRAPHS", "0", "tests/test_fd_gpu.py", "golden_solves or preconditioner_cost"),
+    ("CMG_SCHWARZ_MMA", "1", "tests/test_sem_gpu.py", "schwarz"),
+    ("CMG_COARSE_INV", "0", "tests/test_sem_gpu.py", "kershaw or transfers_and_coarse"),
+    ("CMG_COARSE_DENSE_MAX", "0", "tests/test_sem_gpu.py", "kershaw or transfers_and_coarse"),
+]
+
+
+@pytest.mark.parametrize("var,val,path,sel", VARIANTS, ids=[f"{v}={x}:{os.path.basename(p)}" for v, x, p, _ in VARIANTS])
+def test_variant_parity(var, val, path, sel):
+    env = dict(os.environ, **{var: val})
+    r = subprocess.run([sys.executable, "-m", "pytest", path, "-m", "gpu", "-q", "-x", "-k", sel, "-p", "no:cacheprovider"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
