@@ -20,6 +20,7 @@
 #include <vector>
 
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cusolverDn.h>
 
 #include "cmg_objects.hpp"
@@ -31,6 +32,42 @@ using namespace cmg;
 namespace {
 
 [[noreturn]] void fail(int code, const std::string& m) { throw cmg::Error(code, m); }
+
+// Stream-ordered 32-bit memory operations (driver API, resolved at run time
+// through the runtime's entry-point query; the library links cudart statically)
+using MemOpFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamMemOps {
+  MemOpFn wait = nullptr, write = nullptr;
+};
+const StreamMemOps& memops() {
+  static const StreamMemOps ops = [] {
+    StreamMemOps o;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      o.wait = reinterpret_cast<MemOpFn>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      o.write = reinterpret_cast<MemOpFn>(f);
+    return o;
+  }();
+  return ops;
+}
+bool stream_mem_ops() { return memops().wait && memops().write; }
+// the stream waits until *flag >= v (v counts up)
+void stream_wait(cudaStream_t s, const unsigned* flag, unsigned v) {
+  if (memops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), v,
+                    CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    fail(CMG_ERUNTIME, "sem: cuStreamWaitValue32 failed");
+}
+// *flag = v once the stream's preceding work is complete (with a memory barrier)
+void stream_write(cudaStream_t s, unsigned* flag, unsigned v) {
+  if (memops().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), v,
+                     CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    fail(CMG_ERUNTIME, "sem: cuStreamWriteValue32 failed");
+}
 
 template <class F>
 int guard(F&& f) {
@@ -214,6 +251,7 @@ struct SemLevel final : cmg_op {
     contrib_send.alloc(static_cast<std::size_t>(Ex) * Ey * N1 * N1);
     halo_lo.zero(s);
     contrib_hi.zero(s);
+    peer_setup();
     // assembled diagonal (App. A5) and the padding mask
     {
       DBuf Ld(static_cast<std::size_t>(E) * NP);
@@ -288,7 +326,134 @@ struct SemLevel final : cmg_op {
                         ctx->stream);
   }
 
+  // ---- face exchange over peer memory (no NCCL on the operator path) ----
+  // Each rank IPC-exports double-buffered pack buffers and four flags; K1 of
+  // the rank above reads my packed top layer straight through NVLink and K2
+  // of the rank below reads my bottom-face contributions the same way.  The
+  // handshake is stream-ordered memory operations on the flags (no spinning
+  // kernels): a pack is followed by a flag write into the consumer's memory,
+  // the consumer's stream waits for it before the kernel that reads the peer
+  // buffer, then acknowledges so the producer may reuse that buffer two
+  // exchanges later.  Epochs count exchanges, identical on every rank (SPMD).
+  struct PeerHalo {
+    bool on = false;
+    std::size_t hn = 0, cn = 0;          // doubles per halo / contribution buffer
+    DBuf hsend, csend;                    // local [2][hn], [2][cn] (IPC-exported)
+    unsigned* flags = nullptr;            // local [4]: halo ready, halo ack, contrib ready, contrib ack
+    const double* hsend_dn = nullptr;     // rank below's hsend (mapped)
+    const double* csend_up = nullptr;     // rank above's csend (mapped)
+    unsigned* flags_dn = nullptr;         // rank below's flags (mapped)
+    unsigned* flags_up = nullptr;         // rank above's flags (mapped)
+    std::vector<void*> opened;            // IPC mappings to close
+    unsigned hepoch = 0, cepoch = 0;
+    ~PeerHalo() {
+      for (void* p : opened) cudaIpcCloseMemHandle(p);
+      if (flags) cudaFree(flags);
+    }
+  };
+  PeerHalo peer;
+
+  void peer_setup() {
+    const char* env = std::getenv("CMG_PEER_HALO");
+    if (!distributed() || (env && std::atoi(env) == 0) || !stream_mem_ops()) return;
+    cudaStream_t s = ctx->stream;
+    peer.hn = static_cast<std::size_t>(Ex) * Ey * N * N;
+    peer.cn = static_cast<std::size_t>(Ex) * Ey * (N + 1) * (N + 1);
+    peer.hsend.alloc(2 * peer.hn);
+    peer.csend.alloc(2 * peer.cn);
+    peer.hsend.zero(s);
+    peer.csend.zero(s);
+    CMG_CUDA(cudaMalloc(&peer.flags, 4 * sizeof(unsigned)));
+    CMG_CUDA(cudaMemsetAsync(peer.flags, 0, 4 * sizeof(unsigned), s));
+    // exchange the three IPC handles of every rank (packed into doubles for the allgather)
+    constexpr int HB = 3 * sizeof(cudaIpcMemHandle_t);
+    constexpr int HD = (HB + 7) / 8;
+    std::vector<unsigned char> mine(HD * 8, 0);
+    cudaIpcMemHandle_t h[3];
+    CMG_CUDA(cudaIpcGetMemHandle(&h[0], peer.hsend.p));
+    CMG_CUDA(cudaIpcGetMemHandle(&h[1], peer.csend.p));
+    CMG_CUDA(cudaIpcGetMemHandle(&h[2], peer.flags));
+    std::memcpy(mine.data(), h, HB);
+    const int R = desc.nranks;
+    DBuf dmine(HD), dall(static_cast<std::size_t>(HD) * R);
+    CMG_CUDA(cudaMemcpyAsync(dmine.p, mine.data(), HD * 8, cudaMemcpyHostToDevice, s));
+    ctx->comm->allgather(dmine.p, dall.p, HD, s);
+    std::vector<unsigned char> all(static_cast<std::size_t>(HD) * 8 * R);
+    CMG_CUDA(cudaMemcpyAsync(all.data(), dall.p, all.size(), cudaMemcpyDeviceToHost, s));
+    CMG_CUDA(cudaStreamSynchronize(s));
+    bool ok = true;
+    auto open = [&](int rank, int which) -> void* {
+      cudaIpcMemHandle_t hh;
+      std::memcpy(&hh, all.data() + static_cast<std::size_t>(rank) * HD * 8 + which * sizeof(cudaIpcMemHandle_t),
+                  sizeof(hh));
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, hh, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+        return nullptr;
+      }
+      peer.opened.push_back(p);
+      return p;
+    };
+    if (down() >= 0) {
+      peer.hsend_dn = static_cast<const double*>(open(down(), 0));
+      peer.flags_dn = static_cast<unsigned*>(open(down(), 2));
+    }
+    if (up() >= 0) {
+      peer.csend_up = static_cast<const double*>(open(up(), 1));
+      peer.flags_up = static_cast<unsigned*>(open(up(), 2));
+    }
+    // all ranks switch together (and only once every mapping exists), else all keep NCCL
+    const double mine_ok = ok ? 1.0 : 0.0;
+    CMG_CUDA(cudaMemcpyAsync(dmine.p, &mine_ok, sizeof(double), cudaMemcpyHostToDevice, s));
+    ctx->comm->allreduce_sum(dmine.p, 1, s);
+    double total = 0.0;
+    CMG_CUDA(cudaMemcpyAsync(&total, dmine.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CMG_CUDA(cudaStreamSynchronize(s));
+    peer.on = total == static_cast<double>(R);
+  }
+
+  void run_peer(int mode, int epi, SemArgs& a) {
+    cudaStream_t s = ctx->stream;
+    SemArgs b = a;
+    if (mode == SEM_AX) {  // input halo: my top layer up, the rank below's into my K1
+      const unsigned k = ++peer.hepoch;
+      const double* hs = peer.hsend.p + (k & 1) * peer.hn;
+      if (up() >= 0) {
+        if (k > 2) stream_wait(s, peer.flags + 1, k - 2);  // rank above done with this buffer
+        sem_pack_top(a, a.u, const_cast<double*>(hs), s);
+        stream_write(s, peer.flags_up + 0, k);
+      }
+      if (down() >= 0) {
+        stream_wait(s, peer.flags + 0, k);
+        b.halo_lo = peer.hsend_dn + (k & 1) * peer.hn;
+      }
+      sem_k1(b, mode, epi, s);
+      if (down() >= 0) stream_write(s, peer.flags_dn + 1, k);
+    } else {
+      sem_k1(b, mode, epi, s);
+    }
+    // shell contributions of my bottom face down, the rank above's into my K2
+    const unsigned k = ++peer.cepoch;
+    const double* cs = peer.csend.p + (k & 1) * peer.cn;
+    if (down() >= 0) {
+      if (k > 2) stream_wait(s, peer.flags + 3, k - 2);  // rank below done with this buffer
+      sem_pack_contrib_bottom(a, const_cast<double*>(cs), s);
+      stream_write(s, peer.flags_dn + 2, k);
+    }
+    if (up() >= 0) {
+      stream_wait(s, peer.flags + 2, k);
+      b.contrib_hi = peer.csend_up + (k & 1) * peer.cn;
+    }
+    sem_k2(b, epi, s);
+    if (up() >= 0) stream_write(s, peer.flags_up + 3, k);
+  }
+
   void run(int mode, int epi, SemArgs& a) {
+    if (peer.on) {
+      run_peer(mode, epi, a);
+      return;
+    }
     // split-launch overlap of the face exchanges (below), opt-in: measured 67.5
     // vs 68.3 GDOF-step/s without it at 2 GPUs -- the extra launch tails of the
     // one-layer K1/K2 pieces cost more than the hidden NCCL latency
