@@ -424,6 +424,24 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
     if (greg) k_sem_k1_greg<N, EPI, 2, 8><<<(unsigned)ne, nt, K3Smem<N, EPI, false>::bytes, s>>>(b);
     else k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, nt, K3Smem<N, EPI>::bytes, s>>>(b);
   } else if constexpr (MODE == SEM_AX) {
+    if constexpr (N == 3) {
+      // order 3: the register-factor line kernel, one element (one warp) per
+      // block, as an A/B knob against the packed low-order kernel below
+      static const int g3 = [] {
+        const char* env = std::getenv("CMG_K1_GREG3");
+        if (env && std::atoi(env) == 1) {
+          CMG_CUDA(cudaFuncSetAttribute(k_sem_k1_greg<3, EPI, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)K3Smem<3, EPI, false>::bytes));
+          return 1;
+        }
+        return 0;
+      }();
+      if (g3) {
+        k_sem_k1_greg<3, EPI, 2, 16><<<(unsigned)ne, 32, K3Smem<3, EPI, false>::bytes, s>>>(a);
+        CMG_LAUNCH_CHECK();
+        return;
+      }
+    }
     // low orders (coarse p-levels): several elements per block, k-split columns
     constexpr std::size_t smem = K1Smem<N, EPI>::bytes;
     static bool configured = false;
