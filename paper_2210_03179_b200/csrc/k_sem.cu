@@ -426,7 +426,8 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
   } else if constexpr (MODE == SEM_AX) {
     if constexpr (N == 3) {
       // order 3: the register-factor line kernel, one element (one warp) per
-      // block, as an A/B knob against the packed low-order kernel below
+      // block, as an A/B knob against the packed low-order kernel below --
+      // measured slower (E=64^3 solve 0.308-0.311 vs 0.304 s), so opt-in
       static const int g3 = [] {
         const char* env = std::getenv("CMG_K1_GREG3");
         if (env && std::atoi(env) == 1) {

@@ -14,6 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = [
     ("CMG_K1_GREG", "0", "tests/test_sem_gpu.py", "apply_diag_rhs or sweeps_all_families or pmg_solves"),
     ("CMG_K1_PREFETCH", "0", "tests/test_sem_gpu.py", "sweeps_all_families"),
+    ("CMG_K1_GREG3", "1", "tests/test_sem_gpu.py", "sweeps_all_families or v_cycle or pmg_solves"),
+    ("CMG_PEER_HALO", "0", "tests/test_multigpu.py", "bitwise"),
     ("CMG_SHELL_LEX", "1", "tests/test_sem_gpu.py", "apply_diag_rhs or sweeps_all_families or v_cycle"),
     ("CMG_CGS_FUSE", "0", "tests/test_sem_gpu.py", "pmg_solves"),
     ("CMG_CGS_FUSE", "0", "tests/test_fd_gpu.py", "golden_solves"),
