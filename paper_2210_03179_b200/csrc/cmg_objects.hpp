@@ -53,6 +53,10 @@ struct Comm {
                 int up, int down, cudaStream_t s);
   void exchange(const double* send_a, std::size_t na, int peer_a, double* recv_a,
                 const double* send_b, std::size_t nb, int peer_b, double* recv_b, cudaStream_t s);
+  // one group, both directions: n_up doubles go up (and arrive from below in
+  // recv_lo), n_dn go down (and arrive from above in recv_hi)
+  void shift(const double* send_up, double* recv_lo, std::size_t n_up, const double* send_dn, double* recv_hi,
+             std::size_t n_dn, int up, int down, cudaStream_t s);
 };
 
 }  // namespace cmg

@@ -111,6 +111,22 @@ void Comm::exchange(const double* send_a, std::size_t na, int peer_a, double* re
   CMG_NCCL(api.GroupEnd());
 }
 
+void Comm::shift(const double* send_up, double* recv_lo, std::size_t n_up, const double* send_dn,
+                 double* recv_hi, std::size_t n_dn, int up, int down, cudaStream_t s) {
+  auto c = static_cast<ncclComm_t>(nccl);
+  auto& api = nccl_api();
+  CMG_NCCL(api.GroupStart());
+  if (up >= 0) {
+    CMG_NCCL(api.Send(send_up, n_up, ncclDouble, up, c, s));
+    CMG_NCCL(api.Recv(recv_hi, n_dn, ncclDouble, up, c, s));
+  }
+  if (down >= 0) {
+    CMG_NCCL(api.Send(send_dn, n_dn, ncclDouble, down, c, s));
+    CMG_NCCL(api.Recv(recv_lo, n_up, ncclDouble, down, c, s));
+  }
+  CMG_NCCL(api.GroupEnd());
+}
+
 }  // namespace cmg
 
 extern "C" {

@@ -18,6 +18,22 @@ __device__ __forceinline__ int owner1d_s(int g, int ne, int& oe) {
   return (g - 1) - oe * N;
 }
 
+// r at global box node (ex*N+a-1, ey*N+b-1, ez*N+c-1) of element (ex, ey, ez):
+// owned slots, or the neighbouring slab's planes (SchwarzArgs ghost layouts)
+template <int N>
+__device__ __forceinline__ double box_value(const SchwarzArgs& A, int ex, int ey, int ez, int a, int b, int c) {
+  constexpr int NOS = sem_nos(N);
+  int oex = 0, oey = 0, oez = 0;
+  const int ax = owner1d_s<N>(ex * N + a - 1, A.Ex, oex);
+  const int ay = owner1d_s<N>(ey * N + b - 1, A.Ey, oey);
+  const int az = owner1d_s<N>(ez * N + c - 1, A.Ez, oez);
+  if (ax < 0 || ay < 0 || az < 0) return 0.0;
+  const long col = oex + (long)A.Ex * oey;
+  if (oez < A.z0) return A.rlo[(col * 2 + (az - (N - 2))) * (N * N) + ay * N + ax];
+  if (oez >= A.z0 + A.Ezl) return A.rhi[col * (N * N) + ay * N + ax];
+  return A.r[(col + (long)A.Ex * A.Ey * (oez - A.z0)) * NOS + sem_pos(N, ax, ay, az)];
+}
+
 // one block per element: gather r on the extended box, FDM solve, write the
 // local solution (RAS: the element's own (N+1)^3 nodes; ASM: all (N+3)^3).
 // Each mode product is a set of line contractions: a thread loads one
@@ -34,7 +50,7 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   __shared__ __align__(16) double S[3][PB2];
   __shared__ double lam[3][PB];
   const long e = blockIdx.x;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
   for (int d = 0; d < 3; ++d) {
     const int id = A.sidx[e * 3 + d];
     for (int q = threadIdx.x; q < PB2; q += blockDim.x) S[d][q] = A.S[(long)id * PB2 + q];
@@ -42,14 +58,7 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   }
   for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
     const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
-    int oex = 0, oey = 0, oez = 0;
-    const int ax = owner1d_s<N>(ex * N + a - 1, A.Ex, oex);
-    const int ay = owner1d_s<N>(ey * N + b - 1, A.Ey, oey);
-    const int az = owner1d_s<N>(ez * N + c - 1, A.Ez, oez);
-    double v = 0.0;
-    if (ax >= 0 && ay >= 0 && az >= 0)
-      v = A.r[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * oez)) * NOS + sem_pos(N, ax, ay, az)];
-    u[a + PX * b + PS * c] = v;
+    u[a + PX * b + PS * c] = box_value<N>(A, ex, ey, ez, a, b, c);
   }
   __syncthreads();
   // line l of dimension dim: the other two indices (p, q) = (l % PB, l / PB)
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
   __shared__ double S[3][PB2];
   __shared__ double lam[3][PB];
   const long e = blockIdx.x;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
   for (int d = 0; d < 3; ++d) {
     const int id = A.sidx[e * 3 + d];
     for (int q = threadIdx.x; q < PB2; q += blockDim.x) S[d][q] = A.S[(long)id * PB2 + q];
@@ -213,14 +222,7 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
   }
   for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
     const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
-    int oex = 0, oey = 0, oez = 0;
-    const int ax = owner1d_s<N>(ex * N + a - 1, A.Ex, oex);
-    const int ay = owner1d_s<N>(ey * N + b - 1, A.Ey, oey);
-    const int az = owner1d_s<N>(ez * N + c - 1, A.Ez, oez);
-    double v = 0.0;
-    if (ax >= 0 && ay >= 0 && az >= 0)
-      v = A.r[((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * oez)) * NOS + sem_pos(N, ax, ay, az)];
-    u[a + PX * b + PS * c] = v;
+    u[a + PX * b + PS * c] = box_value<N>(A, ex, ey, ez, a, b, c);
   }
   __syncthreads();
   auto line_base = [](int dim, int l) {
@@ -295,8 +297,8 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
 // ascending-element order, oracle_schwarz.c) and applies W = 1/count
 template <int N>
 __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
-  constexpr int PB = N + 3, PB3 = PB * PB * PB, NOS = sem_nos(N);
-  const long n = (long)A.Ex * A.Ey * A.Ez * NOS;
+  constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, NOS = sem_nos(N);
+  const long n = (long)A.Ex * A.Ey * A.Ezl * NOS;
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) {
     const long e = q / NOS;
     int a, b, c;
@@ -304,7 +306,7 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
       y[q] = 0.0;
       continue;
     }
-    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
     const int gx = ex * N + a + 1, gy = ey * N + b + 1, gz = ez * N + c + 1;
     if (gx >= N * A.Ex || gy >= N * A.Ey || gz >= N * A.Ez) {
       y[q] = 0.0;
@@ -319,9 +321,11 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
         if (cy < 0 || cy >= A.Ey || !(cy * N - 1 <= gy && gy <= cy * N + N + 1)) continue;
         for (int cx = gx / N - 2; cx <= gx / N + 1; ++cx) {
           if (cx < 0 || cx >= A.Ex || !(cx * N - 1 <= gx && gx <= cx * N + N + 1)) continue;
-          const long e2 = cx + (long)A.Ex * (cy + (long)A.Ey * cz);
+          const long col = cx + (long)A.Ex * cy;
           const int la = gx - cx * N + 1, lb = gy - cy * N + 1, lc = gz - cz * N + 1;
-          acc += A.Lout[e2 * PB3 + la + PB * (lb + PB * lc)];
+          if (cz < A.z0) acc += A.Llo[col * PB2 + la + PB * lb];  // lc == N+2
+          else if (cz >= A.z0 + A.Ezl) acc += A.Lhi[(col * 2 + lc) * PB2 + la + PB * lb];  // lc 0, 1
+          else acc += A.Lout[(col + (long)A.Ex * A.Ey * (cz - A.z0)) * PB3 + la + PB * (lb + PB * lc)];
           ++cnt;
         }
       }
@@ -330,10 +334,49 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
   }
 }
 
+// Faces for the neighbouring slabs, in the SchwarzArgs ghost layouts.  what 0:
+// r planes az = N-2, N-1 of the top layer (up) and az = 0 of the bottom layer
+// (dn); what 1: ASM Lout plane z = N+2 of the top layer (up) and z = 0, 1 of
+// the bottom layer (dn).
+template <int N>
+__global__ void k_schwarz_pack(SchwarzArgs A, int what, double* __restrict__ up, double* __restrict__ dn) {
+  constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, NOS = sem_nos(N), NN = N * N;
+  const long cols = (long)A.Ex * A.Ey, top = cols * (A.Ezl - 1);
+  const int pu = what == 0 ? 2 * NN : PB2, pd = what == 0 ? NN : 2 * PB2;
+  const long n = cols * (pu + pd);
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) {
+    const bool isup = q < cols * pu;
+    const long k = isup ? q : q - cols * pu;
+    const int per = isup ? pu : pd;
+    const long col = k / per;
+    const int i = (int)(k - col * per);
+    const long e = (isup ? top : 0) + col;
+    double v;
+    if (what == 0) {  // i = plane * NN + ay * N + ax
+      const int pl = i / NN, ay = (i % NN) / N, ax = i % N;
+      v = A.r[e * NOS + sem_pos(N, ax, ay, isup ? N - 2 + pl : 0)];
+    } else {          // i = plane * PB2 + b * PB + a
+      const int pl = i / PB2;
+      v = A.Lout[e * PB3 + (isup ? N + 2 : pl) * PB2 + i % PB2];
+    }
+    (isup ? up : dn)[k] = v;
+  }
+}
+
 }  // namespace
 
+void sem_schwarz_pack(const SchwarzArgs& a, int what, double* up, double* dn, cudaStream_t s) {
+  const long n = schwarz_ghost_up(a, what) + schwarz_ghost_dn(a, what);
+  const unsigned g = (unsigned)std::min<long>((n + 255) / 256, 148 * 8);
+#define X(nn) \
+  if (a.N == nn) { k_schwarz_pack<nn><<<g, 256, 0, s>>>(a, what, up, dn); CMG_LAUNCH_CHECK(); return; }
+  X(2) X(3) X(4) X(5) X(7)
+#undef X
+  throw Error(EINVAL_, "Schwarz smoother: unsupported order");
+}
+
 void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
-  const long E = (long)a.Ex * a.Ey * a.Ez;
+  const long E = (long)a.Ex * a.Ey * a.Ezl;
   // CUDA-core line contractions by default; the DMMA variant is opt-in
   // (CMG_SCHWARZ_MMA=1): measured 826 vs 562 us per apply at E=32^3 -- the
   // fragment index math and the dependent m8n8k4 chains cost more than the
@@ -355,7 +398,7 @@ void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
 }
 
 void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s) {
-  const long n = (long)a.Ex * a.Ey * a.Ez * sem_nos(a.N);
+  const long n = (long)a.Ex * a.Ey * a.Ezl * sem_nos(a.N);
   unsigned g = (unsigned)std::min<long>((n + 255) / 256, 148 * 16);
 #define X(nn) \
   if (a.N == nn) { k_asm_gather<nn><<<g, 256, 0, s>>>(a, y); CMG_LAUNCH_CHECK(); return; }

@@ -670,6 +670,7 @@ struct cmg_pmg {
   // Schwarz smoother data per smoothed level
   struct Schwarz {
     DBuf S, lam, Lout, wmult;
+    DBuf rsend, rlo, rhi, Lsend, Llo, Lhi;  // slab faces (partitioned levels)
     IBuf sidx;
     cmg_pmg* p = nullptr;
     int level = 0;
@@ -900,7 +901,7 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
 // ---- Schwarz (ASM / RAS) smoother, PAPER.md:560-629 ----
 void schwarz_setup(cmg_pmg* p, int l) {
   SemLevel* L = p->lev[l].get();
-  if (L->distributed()) fail(CMG_EINVAL, "pmg: Schwarz smoothers run on one GPU (BASELINE configs[2])");
+  if (L->N < 2) fail(CMG_EINVAL, "pmg: Schwarz smoothers need order >= 2");
   auto sc = std::make_unique<cmg_pmg::Schwarz>();
   sc->p = p;
   sc->level = l;
@@ -909,14 +910,17 @@ void schwarz_setup(cmg_pmg* p, int l) {
   host_gll(N, xi.data(), w.data());
   host_deriv_matrix(N, xi.data(), D.data());
   const int ne[3] = {L->Ex, L->Ey, L->Ez};
-  // element box lengths
-  std::vector<double> Lel(static_cast<std::size_t>(L->E) * 3);
-  for (long e = 0; e < L->E; ++e) {
-    const int ex = static_cast<int>(e % L->Ex), ey = static_cast<int>((e / L->Ex) % L->Ey),
-              ez = static_cast<int>(e / (static_cast<long>(L->Ex) * L->Ey));
-    host_element_lengths(L->desc.geometry, L->desc.eps, N, xi.data(), L->Ex, L->Ey, L->Ez, ex, ey, ez,
-                         &Lel[e * 3]);
-  }
+  // element box lengths of the owned layers and one neighbouring layer each side
+  const long cols = static_cast<long>(L->Ex) * L->Ey;
+  const int zl = std::max(L->z0 - 1, 0), zh = std::min(L->z1 + 1, L->Ez);
+  std::vector<double> Lel(static_cast<std::size_t>(cols) * (zh - zl) * 3);
+  auto lel = [&](const int* c) { return &Lel[((c[2] - zl) * cols + c[0] + static_cast<long>(L->Ex) * c[1]) * 3]; };
+  for (int ez = zl; ez < zh; ++ez)
+    for (int ey = 0; ey < L->Ey; ++ey)
+      for (int ex = 0; ex < L->Ex; ++ex) {
+        const int c[3] = {ex, ey, ez};
+        host_element_lengths(L->desc.geometry, L->desc.eps, N, xi.data(), L->Ex, L->Ey, L->Ez, ex, ey, ez, lel(c));
+      }
   // 1D FDM bases, deduplicated on (Ll, L, Lr, boundary flags)
   std::map<std::tuple<double, double, double, int>, int> uniq;
   std::vector<double> Sall, lall;
@@ -924,12 +928,14 @@ void schwarz_setup(cmg_pmg* p, int l) {
   std::vector<double> Sd(pb * pb), ld(pb);
   for (long e = 0; e < L->E; ++e) {
     const int ec[3] = {static_cast<int>(e % L->Ex), static_cast<int>((e / L->Ex) % L->Ey),
-                       static_cast<int>(e / (static_cast<long>(L->Ex) * L->Ey))};
+                       L->z0 + static_cast<int>(e / cols)};
     for (int d = 0; d < 3; ++d) {
-      const long stride = d == 0 ? 1 : (d == 1 ? L->Ex : static_cast<long>(L->Ex) * L->Ey);
-      const double Lc = Lel[e * 3 + d];
-      const double Ll = ec[d] > 0 ? Lel[(e - stride) * 3 + d] : Lc;
-      const double Lr = ec[d] + 1 < ne[d] ? Lel[(e + stride) * 3 + d] : Lc;
+      int lo[3] = {ec[0], ec[1], ec[2]}, hi[3] = {ec[0], ec[1], ec[2]};
+      --lo[d];
+      ++hi[d];
+      const double Lc = lel(ec)[d];
+      const double Ll = ec[d] > 0 ? lel(lo)[d] : Lc;
+      const double Lr = ec[d] + 1 < ne[d] ? lel(hi)[d] : Lc;
       const int g0 = ec[d] * N, gmax = N * ne[d];
       const int dl = (g0 - 1) <= 0, d0 = g0 == 0, dN = g0 + N == gmax, dr = (g0 + N + 1) >= gmax;
       const int flags = dl | (d0 << 1) | (dN << 2) | (dr << 3);
@@ -963,6 +969,26 @@ void schwarz_setup(cmg_pmg* p, int l) {
     sem_inverse_diag(L->args(), cnt.p, sc->wmult.p, p->ctx->dflag + 13, p->ctx->stream);
     p->ctx->sync();
   }
+  if (L->distributed()) {
+    SchwarzArgs g;
+    g.N = N;
+    g.Ex = L->Ex;
+    g.Ey = L->Ey;
+    const long ru = schwarz_ghost_up(g, 0), rd = schwarz_ghost_dn(g, 0);
+    sc->rsend.alloc(ru + rd);
+    sc->rlo.alloc(ru);
+    sc->rhi.alloc(rd);
+    sc->rlo.zero(p->ctx->stream);
+    sc->rhi.zero(p->ctx->stream);
+    if (!ras) {
+      const long lu = schwarz_ghost_up(g, 1), ld = schwarz_ghost_dn(g, 1);
+      sc->Lsend.alloc(lu + ld);
+      sc->Llo.alloc(lu);
+      sc->Lhi.alloc(ld);
+      sc->Llo.zero(p->ctx->stream);
+      sc->Lhi.zero(p->ctx->stream);
+    }
+  }
   if (static_cast<int>(p->sch.size()) <= l) p->sch.resize(l + 1);
   p->sch[l] = std::move(sc);
 }
@@ -978,13 +1004,30 @@ void schwarz_apply(void* vctx, const double* r, double* out) {
   a.Ex = L->Ex;
   a.Ey = L->Ey;
   a.Ez = L->Ez;
+  a.z0 = L->z0;
+  a.Ezl = L->Ezl;
   a.S = sc->S.p;
   a.lam = sc->lam.p;
   a.sidx = sc->sidx.p;
   a.r = r;
   a.Lout = sc->Lout.p;
   a.ras = p->smoother == 2;
+  const bool part = L->distributed();
+  if (part) {  // r planes of the neighbouring slabs (NCCL, one group)
+    const long ru = schwarz_ghost_up(a, 0), rd = schwarz_ghost_dn(a, 0);
+    sem_schwarz_pack(a, 0, sc->rsend.p, sc->rsend.p + ru, s);
+    p->ctx->comm->shift(sc->rsend.p, sc->rlo.p, ru, sc->rsend.p + ru, sc->rhi.p, rd, L->up(), L->down(), s);
+    a.rlo = sc->rlo.p;
+    a.rhi = sc->rhi.p;
+  }
   sem_schwarz_local(a, s);
+  if (part && !a.ras) {  // ASM also sums the neighbouring layers' boxes
+    const long lu = schwarz_ghost_up(a, 1), ld = schwarz_ghost_dn(a, 1);
+    sem_schwarz_pack(a, 1, sc->Lsend.p, sc->Lsend.p + lu, s);
+    p->ctx->comm->shift(sc->Lsend.p, sc->Llo.p, lu, sc->Lsend.p + lu, sc->Lhi.p, ld, L->up(), L->down(), s);
+    a.Llo = sc->Llo.p;
+    a.Lhi = sc->Lhi.p;
+  }
   if (a.ras) {
     SemArgs b = L->args();
     b.lvec = sc->Lout.p;

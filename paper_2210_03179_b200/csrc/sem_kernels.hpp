@@ -141,18 +141,41 @@ void coarse_slots_to_dense(const CoarseGrid& g, const double* full, double* b, c
 void coarse_dense_to_slots(const CoarseGrid& g, const double* x, double* ec, cudaStream_t s);
 
 // Schwarz (ASM/RAS) with FDM local solves
-// single-rank (the Schwarz configs are 1-GPU, BASELINE configs[2])
+// On a z-slab partition (layers z0 .. z0+Ezl-1 of Ez) the extended boxes of
+// the first / last owned layer reach two node planes into the layer below and
+// one into the layer above; those planes arrive in rlo / rhi.  ASM also sums
+// the boxes of the neighbouring layers: one Lout plane of the layer below
+// (Llo) and two of the layer above (Lhi).  Ghost layouts:
+//   rlo [Ex*Ey][2][N][N] (az = N-2, N-1)     rhi [Ex*Ey][N][N] (az = 0)
+//   Llo [Ex*Ey][PB][PB]  (box z = N+2)       Lhi [Ex*Ey][2][PB][PB] (box z = 0, 1)
 struct SchwarzArgs {
-  int N = 7, Ex = 1, Ey = 1, Ez = 1;
+  int N = 7, Ex = 1, Ey = 1, Ez = 1;  // Ez: global element layers
+  int z0 = 0, Ezl = 1;                // owned layers
   const double* S = nullptr;    // unique 1D eigenbases [nu][pb*pb] (columns, S^T B S = I)
   const double* lam = nullptr;  // [nu][pb]
   const int* sidx = nullptr;    // [E][3] index of each element's x/y/z basis
   const double* r = nullptr;    // input residual (slots)
   double* Lout = nullptr;       // local solutions (ras: (N+1)^3 per element; asm: (N+3)^3)
+  const double* rlo = nullptr;
+  const double* rhi = nullptr;
+  const double* Llo = nullptr;
+  const double* Lhi = nullptr;
   int ras = 1;
 };
 void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s);
 // ASM: y = W sum_e R_e^T Lout_e  (W = 1/number of covering subdomains)
 void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s);
+// pack the faces the neighbouring slabs need: r planes (what = 0) before the
+// local solves, ASM Lout planes (what = 1) after them
+void sem_schwarz_pack(const SchwarzArgs& a, int what, double* up, double* dn, cudaStream_t s);
+// ghost sizes in doubles: up-going (= rlo / Llo) and down-going (= rhi / Lhi)
+inline long schwarz_ghost_up(const SchwarzArgs& a, int what) {
+  const long pb = a.N + 3;
+  return (long)a.Ex * a.Ey * (what == 0 ? 2L * a.N * a.N : pb * pb);
+}
+inline long schwarz_ghost_dn(const SchwarzArgs& a, int what) {
+  const long pb = a.N + 3;
+  return (long)a.Ex * a.Ey * (what == 0 ? (long)a.N * a.N : 2 * pb * pb);
+}
 
 }  // namespace cmg

@@ -55,6 +55,26 @@ def test_partition_bitwise_identical(tmp_path, geometry):
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("smoother,geometry", [(1, 0), (2, 0), (2, 1)], ids=["asm-box", "ras-box", "ras-kershaw"])
+def test_schwarz_partition_bitwise_identical(tmp_path, smoother, geometry):
+    """Chebyshev-ASM/RAS p-MG(7,3,1) on the z-slab partition: the extended
+    boxes of the first/last owned layer read the neighbouring slabs' node
+    planes (and ASM sums their boxes), so the solve is BITWISE the 1-GPU one
+    (which tests/test_sem_gpu.py checks against the oracle)."""
+    import numpy as np
+
+    extra = ("--smoother", str(smoother), "--geometry", str(geometry), "--kpre", "2")
+    r1 = _run(1, str(tmp_path / "s1.json"), extra)
+    x1 = np.load(str(tmp_path / "s1.json") + ".x.npy")
+    for w in [2] + ([4] if _ngpus() >= 4 else []):
+        rw = _run(w, str(tmp_path / f"s{w}.json"), extra)
+        for k in ("iterations", "fine_matvecs", "history", "lambda"):
+            assert rw[k] == r1[k], (w, k)
+        xw = np.load(str(tmp_path / f"s{w}.json") + ".x.npy")
+        assert np.array_equal(xw, x1), (w, np.max(np.abs(xw - x1)))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
 def test_sweep_across_ranks_matches_single_gpu(tmp_path):
     """harness.hpp:297-337 sweep dealt over 2 ranks (tools/sweep.py): the merged
     CSV (timing column off) is byte-identical to the 1-GPU sweep."""
