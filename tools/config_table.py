@@ -79,6 +79,19 @@ def main():
             P = sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 36, geometry=sem.KERSHAW, eps=eps), (7, 5, 3, 1), ctx=ctx)
             run(f"paper Kershaw eps={eps} E=36^3 (7,5,3,1) [paper PGMRES: {paper_its} its]", P, 0, 3, 3)
             del P
+    if "paper-ras" in only:
+        # PAPER.md tab:fastest_solver_nekrs (:1016-1018, 6x V100): the fastest Chebyshev-RAS
+        # configurations, (7,3,1) p-MG.  1st-kind with the empirically tuned lambda_min is
+        # run here with the default lambda_min (family first).
+        for eps, cases in ((1.0, ((0, 2, 2, "paper 1st lmin-opt RAS(2,2): 0.09 s, 8 its"), (3, 2, 2, ""))),
+                           (0.3, ((0, 5, 5, "paper 1st lmin-opt RAS(5,5): 0.67 s, 28 its"), (3, 12, 0, ""))),
+                           (0.05, ((3, 12, 0, "paper 4th-opt RAS(12,0): 2.40 s, 88 its"), (0, 5, 5, "")))):
+            P = sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 36, geometry=sem.KERSHAW, eps=eps), (7, 3, 1),
+                                 smoother=sem.RAS, ctx=ctx)
+            for fam, kpre, kpost, note in cases:
+                run(f"paper Kershaw eps={eps} E=36^3 (7,3,1) RAS" + (f" [{note}]" if note else ""), P, fam, kpre,
+                    kpost)
+            del P
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as fh:
         json.dump({"device": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%d %H:%M:%S"),

@@ -6,6 +6,7 @@
     python tools/launch_summary.py gpurun_out/tts_launches.csv
 
 --case sem : p-MG(7,3,1)-PGMRES(30), (8,0) 4th-kind half V-cycle, tol 1e-8 (bench.py's time_to_solution)
+--case kras: paper Kershaw eps=0.05, E=36^3, 4th-opt Chebyshev-RAS (12,0), 4 PGMRES iterations
 --case fd  : FD config 1, n=256 PGMRES + (4,0) 4th-kind half V-cycle, tol 1e-6 (bench.py's fd_config1)
 """
 import argparse
@@ -19,7 +20,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--case", default="sem", choices=["sem", "fd", "ras"])
+    ap.add_argument("--case", default="sem", choices=["sem", "fd", "ras", "kras"])
     ap.add_argument("--E", type=int, default=64)
     args = ap.parse_args()
     import torch
@@ -28,7 +29,13 @@ def main():
     from paper_2210_03179_b200 import sem
 
     ctx = cm.Context(0)
-    if args.case == "ras":  # configs[2]: Chebyshev-RAS (1,1), E=32^3
+    if args.case == "kras":  # paper Kershaw eps=0.05 E=36^3, 4th-opt RAS(12,0), first 4 iterations
+        P = sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 36, geometry=sem.KERSHAW, eps=0.05), (7, 3, 1),
+                             smoother=sem.RAS, ctx=ctx)
+        A, b = P.A, P.A.rhs()
+        M = P.preconditioner(cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth_opt, 1, P.lambda_tilde[0]), 12, 0))
+        opts = cm.SolveOptions(tol=1e-8, restart=30, maxit=4)
+    elif args.case == "ras":  # configs[2]: Chebyshev-RAS (1,1), E=32^3
         P = sem.PMGHierarchy(sem.SemDesc(7, 32, 32, 32), (7, 3, 1), smoother=sem.RAS, ctx=ctx)
         A, b = P.A, P.A.rhs()
         M = P.preconditioner(cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 1, 1))
