@@ -84,9 +84,66 @@ __global__ void k_dense_to_slots(int Ex, int Ey, int Ezl, int z0, int nx, int ny
   }
 }
 
+// lower triangle -> upper (potri leaves only the lower half of the symmetric
+// inverse); 32x32 tiles through shared memory so both sides are coalesced
+__global__ void k_symmetrize(long n, double* __restrict__ A) {
+  __shared__ double T[32][33];
+  const int bi = blockIdx.x, bj = blockIdx.y;  // tile (row block bi, column block bj), bi >= bj
+  if (bi < bj) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int c = ty; c < 32; c += 8) {
+    const long i = (long)bi * 32 + tx, j = (long)bj * 32 + c;
+    T[c][tx] = (i < n && j < n) ? A[i + j * n] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const long i = (long)bi * 32 + r, j = (long)bj * 32 + tx;  // write A[j, i] = A[i, j], i > j
+    if (i < n && j < n && i > j) A[j + i * n] = T[tx][r];
+  }
+}
+
+// y[c] = sum_k A[k, c] b[k] for the columns of a column slab: one block per
+// column, fixed per-thread strides and a fixed reduction tree, so every y[c]
+// is the same bits whichever slab (rank) computes it
+__global__ void __launch_bounds__(256) k_coldot(long n, long ncols, const double* __restrict__ A,
+                                                const double* __restrict__ b, double* __restrict__ y) {
+  __shared__ double red[8];
+  for (long c = blockIdx.x; c < ncols; c += gridDim.x) {
+    const double* col = A + c * n;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    long k = threadIdx.x;
+    for (; k + 768 < n; k += 1024) {
+      a0 += col[k] * b[k];
+      a1 += col[k + 256] * b[k + 256];
+      a2 += col[k + 512] * b[k + 512];
+      a3 += col[k + 768] * b[k + 768];
+    }
+    for (; k < n; k += 256) a0 += col[k] * b[k];
+    double v = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      y[c] = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
+    __syncthreads();
+  }
+}
+
 inline unsigned grid_for(long n) { return (unsigned)std::min<long>((n + 255) / 256, 148L * 16); }
 
 }  // namespace
+
+void coarse_symmetrize(long n, double* A, cudaStream_t s) {
+  const unsigned t = (unsigned)((n + 31) / 32);
+  k_symmetrize<<<dim3(t, t), dim3(32, 8), 0, s>>>(n, A);
+  CMG_LAUNCH_CHECK();
+}
+void coarse_coldot(long n, long ncols, const double* A, const double* b, double* y, cudaStream_t s) {
+  if (ncols <= 0) return;
+  k_coldot<<<(unsigned)std::min<long>(ncols, 148L * 8), 256, 0, s>>>(n, ncols, A, b, y);
+  CMG_LAUNCH_CHECK();
+}
 
 void coarse_probe(const CoarseGrid& g, int cx, int cy, int cz, double* v, cudaStream_t s) {
   k_probe<<<grid_for((long)g.Ex * g.Ey * g.Ezl), 256, 0, s>>>(g.Ex, g.Ey, g.Ezl, g.z0, g.nx, g.ny, g.nz, cx, cy, cz,

@@ -19,7 +19,6 @@
 #include <string>
 #include <vector>
 
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cusolverDn.h>
 
@@ -679,13 +678,14 @@ struct cmg_pmg {
   int cnx = 0, cny = 0, cnz = 0;
   // dense Cholesky factor of the deformed-mesh p=1 operator (k_sem_coarse.cu)
   cusolverDnHandle_t sol = nullptr;
-  cublasHandle_t blas = nullptr;  // set when the explicit inverse is used
+  DBuf cS;                        // explicit inverse: this rank's column slab [cu0, cu1)
+  long cu0 = 0, cu1 = 0;
+  bool cinv = false;
   DBuf cA, cwork, cb, cx;
   int* cinfo = nullptr;
   int cn = 0;
   ~cmg_pmg() {
     if (sol) cusolverDnDestroy(sol);
-    if (blas) cublasDestroy(blas);
     if (cinfo) cudaFree(cinfo);
   }
 };
@@ -794,10 +794,9 @@ void coarse_dense_setup(cmg_pmg* p) {
   if (info != 0) fail(CMG_ERUNTIME, "pmg: coarse p=1 operator not positive definite");
   p->cb.alloc(n);
   p->cn = static_cast<int>(n);
-  // Default: form the inverse from the factor once (potri) and apply it as one
-  // symmetric matrix-vector product per coarse solve -- a single bandwidth-bound
-  // pass over the lower triangle instead of two latency-bound triangular
-  // solves.  CMG_COARSE_INV=0 keeps potrs.
+  // Default: form the inverse from the factor once (potri) and apply it as
+  // column dot products per coarse solve -- a bandwidth-bound pass instead of
+  // two latency-bound triangular solves.  CMG_COARSE_INV=0 keeps potrs.
   const char* inv_env = std::getenv("CMG_COARSE_INV");
   if (inv_env && std::atoi(inv_env) == 0) return;
   int lw2 = 0;
@@ -811,9 +810,26 @@ void coarse_dense_setup(cmg_pmg* p) {
   CMG_CUDA(cudaMemcpyAsync(&info, p->cinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
   CMG_CUDA(cudaStreamSynchronize(s));
   if (info != 0) fail(CMG_ERUNTIME, "pmg: coarse inverse failed");
-  if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) fail(CMG_ERUNTIME, "pmg: cublasCreate failed");
-  cublasSetStream(p->blas, s);
-  cublasSetPointerMode(p->blas, CUBLAS_POINTER_MODE_HOST);
+  // Keep only the columns of the (symmetric) inverse whose unknowns this rank
+  // owns: p=1 unknown (ix, iy, iz) lives in element layer iz, so a z-slab's
+  // unknowns are one contiguous column range and each rank reads n x (its
+  // unknowns) per coarse solve instead of the whole matrix.
+  coarse_symmetrize(n, p->cA.p, s);
+  const long layer = static_cast<long>(p->cnx) * p->cny;
+  p->cu0 = std::min<long>(n, layer * C->z0);
+  p->cu1 = std::min<long>(n, layer * (C->z0 + C->Ezl));
+  if (p->cu0 == 0 && p->cu1 == n) {  // one rank: the slab is the whole matrix
+    std::swap(p->cS.p, p->cA.p);
+    std::swap(p->cS.n, p->cA.n);
+  } else {
+    p->cS.alloc(static_cast<std::size_t>(n) * std::max<long>(p->cu1 - p->cu0, 1));
+    CMG_CUDA(cudaMemcpyAsync(p->cS.p, p->cA.p + p->cu0 * n,
+                             static_cast<std::size_t>(n) * (p->cu1 - p->cu0) * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+    CMG_CUDA(cudaStreamSynchronize(s));
+  }
+  p->cA.release();
+  p->cinv = true;
   p->cx.alloc(n);
 }
 
@@ -837,11 +853,8 @@ void pmg_coarse_solve(cmg_pmg* p, const double* rc, double* ec) {
     }
     const CoarseGrid g{c->Ex, c->Ey, c->Ezl, c->z0, p->cnx, p->cny, p->cnz};
     coarse_slots_to_dense(g, in, p->cb.p, s);
-    if (p->blas) {  // x = A^{-1} b with the symmetric inverse's lower triangle (one HBM pass)
-      const double one = 1.0, zero = 0.0;
-      if (cublasDsymv(p->blas, CUBLAS_FILL_MODE_LOWER, p->cn, &one, p->cA.p, p->cn, p->cb.p, 1, &zero, p->cx.p, 1) !=
-          CUBLAS_STATUS_SUCCESS)
-        fail(CMG_ERUNTIME, "pmg: coarse symv failed");
+    if (p->cinv) {  // x = A^{-1} b on this rank's unknowns: one HBM pass over its column slab
+      coarse_coldot(p->cn, p->cu1 - p->cu0, p->cS.p, p->cb.p, p->cx.p + p->cu0, s);
       coarse_dense_to_slots(g, p->cx.p, ec, s);
       return;
     }

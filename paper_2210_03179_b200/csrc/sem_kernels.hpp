@@ -139,6 +139,10 @@ void coarse_probe_extract(const CoarseGrid& g, int cx, int cy, int cz, const dou
 void coarse_dense_build(const CoarseGrid& g, const double* rows, double* A, cudaStream_t s);
 void coarse_slots_to_dense(const CoarseGrid& g, const double* full, double* b, cudaStream_t s);
 void coarse_dense_to_slots(const CoarseGrid& g, const double* x, double* ec, cudaStream_t s);
+// n x n lower triangle -> full symmetric (column-major)
+void coarse_symmetrize(long n, double* A, cudaStream_t s);
+// y[c] = A[:, c] . b for the ncols columns of a column-major n x ncols slab (deterministic)
+void coarse_coldot(long n, long ncols, const double* A, const double* b, double* y, cudaStream_t s);
 
 // Schwarz (ASM/RAS) with FDM local solves
 // On a z-slab partition (layers z0 .. z0+Ezl-1 of Ez) the extended boxes of
