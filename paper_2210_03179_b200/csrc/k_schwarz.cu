@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
     const int p = l % PB, q = l / PB;
     return dim == 0 ? PX * p + PS * q : (dim == 1 ? p + PS * q : p + PX * q);
   };
-  constexpr int STRIDE[3] = {1, PX, PS};
+  auto stride_of = [](int dim) { return dim == 0 ? 1 : (dim == 1 ? PX : PS); };
   // Two lines per thread share every eigenbasis load (the broadcast loads of
   // S dominate the shared-memory traffic), and S is read two entries at a time
   // when PB is even.  Every output still sums its PB terms in ascending order.
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
     for (int l = threadIdx.x; l < HALF; l += blockDim.x) {
       const int l2 = l + HALF;
       const bool two = l2 < PB2;
-      const int b1 = line_base(dim, l), b2 = line_base(dim, two ? l2 : l), st = STRIDE[dim];
+      const int b1 = line_base(dim, l), b2 = line_base(dim, two ? l2 : l), st = stride_of(dim);
       double v1[PB], v2[PB];
 #pragma unroll
       for (int m = 0; m < PB; ++m) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
     for (int l = threadIdx.x; l < HALF; l += blockDim.x) {
       const int l2 = l + HALF;
       const bool two = l2 < PB2;
-      const int b1 = line_base(dim, l), b2 = line_base(dim, two ? l2 : l), st = STRIDE[dim];
+      const int b1 = line_base(dim, l), b2 = line_base(dim, two ? l2 : l), st = stride_of(dim);
       double v1[PB], v2[PB];
 #pragma unroll
       for (int m = 0; m < PB; ++m) {
@@ -193,6 +193,114 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   }
 }
 
+// Low orders (N <= 4, the p=3 level of the (7,3,1) Schwarz schedule): a box
+// has only (N+3)^2 <= 49 lines per pass, so one element per block left most
+// threads idle.  EPB elements share a block, one line per thread; every
+// output is formed by exactly the same expression sequence as above, so the
+// two kernels give identical bits.
+template <int N, int EPB>
+__global__ void __launch_bounds__(EPB * (N + 3) * (N + 3)) k_schwarz_local_small(SchwarzArgs A, long E) {
+  constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, N1 = N + 1;
+  constexpr int PX = PB | 1, PS = PX * PB, BOX = PS * PB;
+  constexpr bool PAIR = PB % 2 == 0;
+  __shared__ double u[EPB][BOX], t[EPB][BOX];
+  __shared__ __align__(16) double S[EPB][3][PB2];
+  __shared__ double lam[EPB][3][PB];
+  const int le = threadIdx.x / PB2, l = threadIdx.x - le * PB2;
+  const long e = blockIdx.x * (long)EPB + le;
+  const bool on = e < E;
+  if (on) {
+    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int id = A.sidx[e * 3 + d];
+      S[le][d][l] = A.S[(long)id * PB2 + l];
+      if (l < PB) lam[le][d][l] = A.lam[(long)id * PB + l];
+    }
+    const int a = l % PB, b = l / PB;
+#pragma unroll
+    for (int c = 0; c < PB; ++c) u[le][a + PX * b + PS * c] = box_value<N>(A, ex, ey, ez, a, b, c);
+  }
+  __syncthreads();
+  double* in = u[le];
+  double* out = t[le];
+  const int p = l % PB, q = l / PB;
+#pragma unroll 1
+  for (int pass = 0; pass < 6; ++pass) {
+    const int dim = pass % 3;
+    const double* Sd = S[le][dim];
+    const int b1 = dim == 0 ? PX * p + PS * q : (dim == 1 ? p + PS * q : p + PX * q);
+    const int st = dim == 0 ? 1 : (dim == 1 ? PX : PS);
+    if (on) {
+      double v[PB];
+#pragma unroll
+      for (int m = 0; m < PB; ++m) v[m] = in[b1 + m * st];
+      if (pass < 3) {  // forward: S^T along dim; the eigenvalue division fused into the last pass
+        if constexpr (PAIR) {
+#pragma unroll
+          for (int o = 0; o < PB; o += 2) {
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < PB; ++m) {
+              const double2 sp = *reinterpret_cast<const double2*>(Sd + m * PB + o);
+              a0 += sp.x * v[m];
+              a1 += sp.y * v[m];
+            }
+            if (pass == 2) {
+              a0 /= (lam[le][0][p] + lam[le][1][q] + lam[le][2][o]);
+              a1 /= (lam[le][0][p] + lam[le][1][q] + lam[le][2][o + 1]);
+            }
+            out[b1 + o * st] = a0;
+            out[b1 + (o + 1) * st] = a1;
+          }
+        } else {
+#pragma unroll
+          for (int o = 0; o < PB; ++o) {
+            double a0 = 0.0;
+#pragma unroll
+            for (int m = 0; m < PB; ++m) a0 += Sd[m * PB + o] * v[m];
+            if (pass == 2) a0 /= (lam[le][0][p] + lam[le][1][q] + lam[le][2][o]);
+            out[b1 + o * st] = a0;
+          }
+        }
+      } else {  // backward: S along dim
+#pragma unroll
+        for (int o = 0; o < PB; ++o) {
+          double a0 = 0.0;
+          if constexpr (PAIR) {
+#pragma unroll
+            for (int m = 0; m < PB; m += 2) {
+              const double2 sp = *reinterpret_cast<const double2*>(Sd + o * PB + m);
+              a0 += sp.x * v[m];
+              a0 += sp.y * v[m + 1];
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < PB; ++m) a0 += Sd[o * PB + m] * v[m];
+          }
+          out[b1 + o * st] = a0;
+        }
+      }
+    }
+    __syncthreads();
+    double* tmp = in;
+    in = out;
+    out = tmp;
+  }
+  if (!on) return;
+  if (A.ras) {
+    for (int r = l; r < N1 * N1 * N1; r += PB2) {
+      const int i = r % N1, j = (r / N1) % N1, k = r / (N1 * N1);
+      A.Lout[e * (N1 * N1 * N1) + r] = in[(i + 1) + PX * (j + 1) + PS * (k + 1)];
+    }
+  } else {
+    for (int r = l; r < PB3; r += PB2) {
+      const int a = r % PB, b = (r / PB) % PB, c = r / PB2;
+      A.Lout[e * PB3 + r] = in[a + PX * b + PS * c];
+    }
+  }
+}
+
 // FP64 tensor-core variant of the same local solve.  Each of the six mode
 // products is a small GEMM  out[o, line] = sum_m M(o, m) in[m, line]  with
 // M = S^T (forward) or S (backward), (N+3) x (N+3) padded to 16 x 12, and the
@@ -229,7 +337,7 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
     const int p = l % PB, q = l / PB;
     return dim == 0 ? PX * p + PS * q : (dim == 1 ? p + PS * q : p + PX * q);
   };
-  constexpr int STRIDE[3] = {1, PX, PS};
+  auto stride_of = [](int dim) { return dim == 0 ? 1 : (dim == 1 ? PX : PS); };
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tg = lane & 3;  // fragment row group / thread in group
   double* in = u;
@@ -238,7 +346,7 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
   for (int pass = 0; pass < 6; ++pass) {
     const int dim = pass % 3;
     const bool fwd = pass < 3;
-    const int st = STRIDE[dim];
+    const int st = stride_of(dim);
     // A fragments (row o, col m) of M for every (m-tile, k-step)
     double af[MT][KT];
 #pragma unroll
@@ -385,6 +493,19 @@ void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
     const char* env = std::getenv("CMG_SCHWARZ_MMA");
     return env && std::atoi(env) == 1;
   }();
+  // low orders: several elements per block (CMG_SCHWARZ_SMALL=0 keeps one per block)
+  static const bool small = [] {
+    const char* env = std::getenv("CMG_SCHWARZ_SMALL");
+    return !(env && std::atoi(env) == 0);
+  }();
+#define XS(n, epb)                                                                              \
+  if (a.N == n && small && !use_mma) {                                                          \
+    k_schwarz_local_small<n, epb><<<(unsigned)((E + epb - 1) / epb), epb * (n + 3) * (n + 3), 0, s>>>(a, E); \
+    CMG_LAUNCH_CHECK();                                                                         \
+    return;                                                                                     \
+  }
+  XS(2, 8) XS(3, 8) XS(4, 4)
+#undef XS
 #define X(n)                                                                  \
   if (a.N == n) {                                                             \
     if (use_mma) k_schwarz_local_mma<n><<<(unsigned)E, 128, 0, s>>>(a);      \
