@@ -201,7 +201,7 @@ void chebyshev_smooth(cmg_op* A, const double* invd, const cmg_cheb_config& cfg,
 // smoothers.hpp:95-148 with the diagonal S replaced by an operator (Schwarz):
 // same recurrences and coefficients as chebyshev_smooth, unfused.
 void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& cfg, std::size_t order,
-                        const double* b, double* x, bool x_is_zero) {
+                        const double* b, double* x, bool x_is_zero, SUpdate U) {
   if (order == 0) return;
   validate_cheb(cfg);
   A->ensure_scratch();
@@ -236,8 +236,12 @@ void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& 
       const double fi = static_cast<double>(it);
       const double c1 = (2.0 * fi - 1.0) / (2.0 * fi + 3.0);
       const double c2 = (8.0 * fi + 4.0) / (2.0 * fi + 3.0) * inv_lmax;
-      S(sctx, r, sv);
-      launch_lincomb(L, c1, d, c2, sv, d, s);
+      if (U) {
+        U(sctx, 4, r, c1, c2, d, r);
+      } else {
+        S(sctx, r, sv);
+        launch_lincomb(L, c1, d, c2, sv, d, s);
+      }
     }
     vec_final_update(L, beta ? beta[order - 1] : 1.0, xz, d, x, s);
   } else {  // smoothers.hpp:95-120
@@ -252,10 +256,14 @@ void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& 
       else launch_axpy(L, 1.0, d, x, s);
       xz = false;
       A->apply(d, t);
-      S(sctx, t, sv);
-      launch_axpy(L, -1.0, sv, r, s);
       const double rho = 1.0 / (2.0 * sigma - rho_prev);
-      launch_lincomb(L, rho * rho_prev, d, 2.0 * rho / delta, r, d, s);
+      if (U) {
+        U(sctx, 1, t, rho * rho_prev, 2.0 * rho / delta, d, r);
+      } else {
+        S(sctx, t, sv);
+        launch_axpy(L, -1.0, sv, r, s);
+        launch_lincomb(L, rho * rho_prev, d, 2.0 * rho / delta, r, d, s);
+      }
       rho_prev = rho;
     }
     vec_final_update(L, 1.0, xz, d, x, s);

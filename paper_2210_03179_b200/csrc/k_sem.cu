@@ -81,8 +81,8 @@ __device__ __forceinline__ int owner1d(int ec, int l, int ne, int& oe) {
 // ---------------------------------------------------------------- epilogues
 template <int EPI>
 struct EpiOps {  // slot-vector operands read for interior nodes, in smem order
-  static constexpr int n = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) ? 3
-                           : (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) ? 2
+  static constexpr int n = (EPI == EPI_CHEB4 || EPI == EPI_CHEB1 || EPI == EPI_SUPD1) ? 3
+                           : (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT || EPI == EPI_SUPD4) ? 2
                            : (EPI == EPI_RESID || EPI == EPI_ADD) ? 1 : 0;
 };
 
@@ -92,6 +92,8 @@ __device__ __forceinline__ const double* epi_op(const SemArgs& A, int q) {
   else if constexpr (EPI == EPI_CHEB1) return q == 0 ? A.x : (q == 1 ? A.r : A.invd);
   else if constexpr (EPI == EPI_CHEB4_INIT || EPI == EPI_CHEB1_INIT) return q == 0 ? A.b : A.invd;
   else if constexpr (EPI == EPI_RESID) return A.b;
+  else if constexpr (EPI == EPI_SUPD4) return q == 0 ? A.invd : A.d;
+  else if constexpr (EPI == EPI_SUPD1) return q == 0 ? A.r_in : (q == 1 ? A.invd : A.d);
   else return A.y;
 }
 
@@ -137,6 +139,12 @@ __device__ __forceinline__ void epilogue(const SemArgs& A, long slot, double w, 
     const double zv = (o0 - w) * o1;
     A.r[slot] = zv;
     A.d_out[slot] = zv / A.theta;
+  } else if constexpr (EPI == EPI_SUPD4) {
+    A.d_out[slot] = A.c1 * o1 + A.c2 * (o0 * w);
+  } else if constexpr (EPI == EPI_SUPD1) {
+    const double rv = o0 - o1 * w;
+    A.r[slot] = rv;
+    A.d_out[slot] = A.c1 * o2 + A.c2 * rv;
   }
 }
 
@@ -307,10 +315,11 @@ __global__ void k_sem_k1_lvec(SemArgs A) {
   const double v = A.lvec[e * NP + l];
   if (i >= 1 && i < N && j >= 1 && j < N && k >= 1 && k < N) {
     const long slot = e * NOS + (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
-    double o0 = 0.0, o1 = 0.0;
+    double o0 = 0.0, o1 = 0.0, o2 = 0.0;
     if constexpr (EpiOps<EPI>::n > 0) o0 = epi_op<EPI>(A, 0)[slot];
     if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
-    epilogue<EPI>(A, slot, v, 0.0, o0, o1, 0.0);
+    if constexpr (EpiOps<EPI>::n > 2) o2 = epi_op<EPI>(A, 2)[slot];
+    epilogue<EPI>(A, slot, v, 0.0, o0, o1, o2);
   } else {
     A.shell[e * A.nshell + A.lut[l]] = v;
   }
@@ -374,6 +383,7 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
   } else {
     if constexpr (EpiOps<EPI>::n > 0) o0 = epi_op<EPI>(A, 0)[slot];
     if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
+    if constexpr (EpiOps<EPI>::n > 2) o2 = epi_op<EPI>(A, 2)[slot];
   }
   epilogue<EPI>(A, slot, sum, dv, o0, o1, o2);
 }
@@ -490,7 +500,9 @@ void dispatch_k1(const SemArgs& a, int mode, int epi, cudaStream_t s) {
   if (mode == SEM_AX) dispatch_k1_epi<N, SEM_AX>(a, epi, s);
   else if (epi == EPI_STORE) launch_k1<N, SEM_LVEC, EPI_STORE>(a, s);
   else if (epi == EPI_ADD) launch_k1<N, SEM_LVEC, EPI_ADD>(a, s);
-  else throw Error(EINVAL_, "sem_k1: LVEC mode supports STORE/ADD");
+  else if (epi == EPI_SUPD4) launch_k1<N, SEM_LVEC, EPI_SUPD4>(a, s);
+  else if (epi == EPI_SUPD1) launch_k1<N, SEM_LVEC, EPI_SUPD1>(a, s);
+  else throw Error(EINVAL_, "sem_k1: LVEC mode supports STORE/ADD/SUPD");
 }
 
 template <int N>
@@ -503,6 +515,8 @@ void dispatch_k2(const SemArgs& a, int epi, cudaStream_t s) {
     case EPI_CHEB1: return launch_k2<N, EPI_CHEB1>(a, s);
     case EPI_CHEB4_INIT: return launch_k2<N, EPI_CHEB4_INIT>(a, s);
     case EPI_CHEB1_INIT: return launch_k2<N, EPI_CHEB1_INIT>(a, s);
+    case EPI_SUPD4: return launch_k2<N, EPI_SUPD4>(a, s);
+    case EPI_SUPD1: return launch_k2<N, EPI_SUPD1>(a, s);
   }
   throw Error(EINVAL_, "sem_k2: bad epilogue");
 }

@@ -1006,9 +1006,18 @@ void schwarz_setup(cmg_pmg* p, int l) {
   p->sch[l] = std::move(sc);
 }
 
-// out = S_ASM r or S_RAS r on level l
-void schwarz_apply(void* vctx, const double* r, double* out) {
-  auto* sc = static_cast<cmg_pmg::Schwarz*>(vctx);
+// CMG_SCHWARZ_FUSE=0: S stored, then separate vector updates
+bool fused_supd() {
+  static const bool on = [] {
+    const char* env = std::getenv("CMG_SCHWARZ_FUSE");
+    return !(env && std::atoi(env) == 0);
+  }();
+  return on;
+}
+
+// local solves of S applied to r on level l (exchanging the neighbour slabs'
+// planes when partitioned); returns the args for the assembly
+SchwarzArgs schwarz_local(cmg_pmg::Schwarz* sc, const double* r) {
   cmg_pmg* p = sc->p;
   SemLevel* L = p->lev[sc->level].get();
   cudaStream_t s = p->ctx->stream;
@@ -1041,6 +1050,16 @@ void schwarz_apply(void* vctx, const double* r, double* out) {
     a.Llo = sc->Llo.p;
     a.Lhi = sc->Lhi.p;
   }
+  return a;
+}
+
+// out = S_ASM r or S_RAS r on level l
+void schwarz_apply(void* vctx, const double* r, double* out) {
+  auto* sc = static_cast<cmg_pmg::Schwarz*>(vctx);
+  cmg_pmg* p = sc->p;
+  SemLevel* L = p->lev[sc->level].get();
+  cudaStream_t s = p->ctx->stream;
+  const SchwarzArgs a = schwarz_local(sc, r);
   if (a.ras) {
     SemArgs b = L->args();
     b.lvec = sc->Lout.p;
@@ -1052,10 +1071,46 @@ void schwarz_apply(void* vctx, const double* r, double* out) {
   }
 }
 
+// Chebyshev-Schwarz recurrence updates (chebyshev_smooth_S).  RAS: the
+// 1/multiplicity scaling and the vector update run in the epilogue of the
+// assembly of the local solutions (EPI_SUPD4 / EPI_SUPD1), so S r is never
+// stored.  ASM: S into scratch, then the vector updates.
+void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2, double* d, double* r) {
+  auto* sc = static_cast<cmg_pmg::Schwarz*>(vctx);
+  cmg_pmg* p = sc->p;
+  SemLevel* L = p->lev[sc->level].get();
+  cudaStream_t s = p->ctx->stream;
+  if (p->smoother == 2) {
+    schwarz_local(sc, in);
+    SemArgs b = L->args();
+    b.lvec = sc->Lout.p;
+    b.invd = sc->wmult.p;
+    b.d = d;
+    b.d_out = d;
+    b.c1 = c1;
+    b.c2 = c2;
+    if (kind == 1) {
+      b.r_in = r;
+      b.r = r;
+    }
+    L->run(SEM_LVEC, kind == 4 ? EPI_SUPD4 : EPI_SUPD1, b);
+    return;
+  }
+  double* sv = p->ctx->workspace(7, L->len);
+  schwarz_apply(vctx, in, sv);
+  if (kind == 4) {
+    launch_lincomb(L->len, c1, d, c2, sv, d, s);
+  } else {
+    launch_axpy(L->len, -1.0, sv, r, s);
+    launch_lincomb(L->len, c1, d, c2, r, d, s);
+  }
+}
+
 void pmg_smooth(cmg_pmg* p, int l, const cmg_cheb_config& cfg, std::size_t order, const double* b,
                 double* x, bool xz) {
   if (p->smoother == 0) chebyshev_smooth(p->lev[l].get(), p->invd[l]->p, cfg, order, b, x, xz);
-  else chebyshev_smooth_S(p->lev[l].get(), schwarz_apply, p->sch[l].get(), cfg, order, b, x, xz);
+  else chebyshev_smooth_S(p->lev[l].get(), schwarz_apply, p->sch[l].get(), cfg, order, b, x, xz,
+                          fused_supd() ? schwarz_update : nullptr);
 }
 
 // multigrid.hpp:69-90, recursively over the p-levels

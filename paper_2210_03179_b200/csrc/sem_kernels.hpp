@@ -29,7 +29,11 @@ enum SemEpi : int {
   EPI_CHEB1 = 3,      // x += d ; z -= invd w ; d_out = c1 d + c2 z
   EPI_CHEB4_INIT = 4, // r = b - w ; d_out = c0 invd r
   EPI_CHEB1_INIT = 5, // z = invd (b - w) ; d_out = z / theta
-  EPI_ADD = 6         // y += w
+  EPI_ADD = 6,        // y += w
+  // Chebyshev-Schwarz (RAS) updates fused into the assembly of the local
+  // solutions (L-vector mode), invd = 1/multiplicity:
+  EPI_SUPD4 = 7,      // d_out = c1 d + c2 (invd w)             (4th kind: d = c1 d + c2 S r)
+  EPI_SUPD1 = 8       // r = r_in - invd w ; d_out = c1 d + c2 r (1st kind: r -= S t; d = c1 d + c2 r)
 };
 
 // K2 contributor table row: [count | a<<8 | b<<16 | c<<24], then per contribution
