@@ -228,22 +228,29 @@ void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& 
     launch_scal_copy(L, nullptr, (4.0 / 3.0) * inv_lmax, sv, d, s);
     for (std::size_t it = 1; it < order; ++it) {
       const double bi = beta ? beta[it - 1] : 1.0;
+      const double fi = static_cast<double>(it);
+      const double c1 = (2.0 * fi - 1.0) / (2.0 * fi + 3.0);
+      const double c2 = (8.0 * fi + 4.0) / (2.0 * fi + 3.0) * inv_lmax;
+      if (U) {
+        // x += beta d ; r -= A d in the operator's fused step epilogue (its d
+        // update reduced to a copy, c1 = 1, c2 = 0), then the S update
+        double* d2 = d == A->s_d.p ? A->s_d2.p : A->s_d.p;
+        A->cheb4_step(bi, 1.0, 0.0, xz, d, r, x, r, d, d2, 0.0);
+        d = d2;
+        xz = false;
+        U(sctx, 4, r, c1, c2, d, r);
+        continue;
+      }
       if (xz) launch_scal_copy(L, nullptr, bi, d, x, s);
       else launch_axpy(L, bi, d, x, s);
       xz = false;
       A->apply(d, t);
       launch_axpy(L, -1.0, t, r, s);
-      const double fi = static_cast<double>(it);
-      const double c1 = (2.0 * fi - 1.0) / (2.0 * fi + 3.0);
-      const double c2 = (8.0 * fi + 4.0) / (2.0 * fi + 3.0) * inv_lmax;
-      if (U) {
-        U(sctx, 4, r, c1, c2, d, r);
-      } else {
-        S(sctx, r, sv);
-        launch_lincomb(L, c1, d, c2, sv, d, s);
-      }
+      S(sctx, r, sv);
+      launch_lincomb(L, c1, d, c2, sv, d, s);
     }
     vec_final_update(L, beta ? beta[order - 1] : 1.0, xz, d, x, s);
+    if (d != A->s_d.p) std::swap(A->s_d.p, A->s_d2.p);
   } else {  // smoothers.hpp:95-120
     const double lmin = cfg.lambda_min_multiplier * cfg.lambda_tilde;
     const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma = theta / delta;

@@ -5,9 +5,10 @@
 // entries are recovered from 27 matrix-free applications with "colour" probe
 // vectors (vertex (ix,iy,iz) has colour (ix%3, iy%3, iz%3); two vertices of
 // one colour are never neighbours).  The rows are scattered into a dense
-// column-major matrix, factored once by Cholesky and every coarse solve is
-// two triangular solves -- exact, like the reference's banded Cholesky
-// (cholesky.hpp:18-91), and deterministic.
+// column-major matrix and factored once by Cholesky; the inverse is formed
+// once, and every coarse solve is a pass of column dot products over the
+// rank's slab of it (or, CMG_COARSE_INV=0, two triangular solves) -- exact,
+// like the reference's banded Cholesky (cholesky.hpp:18-91), and deterministic.
 #include <algorithm>
 
 #include "sem_kernels.hpp"
@@ -104,30 +105,33 @@ __global__ void k_symmetrize(long n, double* __restrict__ A) {
 
 // y[c] = sum_k A[k, c] b[k] for the columns of a column slab: one block per
 // column, fixed per-thread strides and a fixed reduction tree, so every y[c]
-// is the same bits whichever slab (rank) computes it
-__global__ void __launch_bounds__(256) k_coldot(long n, long ncols, const double* __restrict__ A,
-                                                const double* __restrict__ b, double* __restrict__ y) {
+// is the same bits whichever slab (rank) computes it.  Eight independent
+// loads in flight per thread (ncu: the 4-load, column-looping version sat at
+// 67% of DRAM bandwidth on long-scoreboard stalls).
+__global__ void __launch_bounds__(256) k_coldot(long n, const double* __restrict__ A, const double* __restrict__ b,
+                                                double* __restrict__ y) {
   __shared__ double red[8];
-  for (long c = blockIdx.x; c < ncols; c += gridDim.x) {
-    const double* col = A + c * n;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    long k = threadIdx.x;
-    for (; k + 768 < n; k += 1024) {
-      a0 += col[k] * b[k];
-      a1 += col[k + 256] * b[k + 256];
-      a2 += col[k + 512] * b[k + 512];
-      a3 += col[k + 768] * b[k + 768];
-    }
-    for (; k < n; k += 256) a0 += col[k] * b[k];
-    double v = (a0 + a1) + (a2 + a3);
+  const long c = blockIdx.x;
+  const double* col = A + c * n;
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  long k = threadIdx.x;
+  for (; k + 7 * 256 < n; k += 8 * 256) {
+    double a[8], v[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0)
-      y[c] = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
-    __syncthreads();
+    for (int u = 0; u < 8; ++u) {
+      a[u] = __ldcs(col + k + u * 256);  // streamed once: keep b in L2 instead
+      v[u] = __ldg(b + k + u * 256);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += a[u] * v[u];
   }
+  for (; k < n; k += 256) acc[0] += col[k] * b[k];
+  double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) y[c] = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
 }
 
 inline unsigned grid_for(long n) { return (unsigned)std::min<long>((n + 255) / 256, 148L * 16); }
@@ -141,7 +145,7 @@ void coarse_symmetrize(long n, double* A, cudaStream_t s) {
 }
 void coarse_coldot(long n, long ncols, const double* A, const double* b, double* y, cudaStream_t s) {
   if (ncols <= 0) return;
-  k_coldot<<<(unsigned)std::min<long>(ncols, 148L * 8), 256, 0, s>>>(n, ncols, A, b, y);
+  k_coldot<<<(unsigned)ncols, 256, 0, s>>>(n, A, b, y);
   CMG_LAUNCH_CHECK();
 }
 
