@@ -402,22 +402,36 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
 }
 
 // ASM: every owned slot sums the extended local solutions covering it (fixed
-// ascending-element order, oracle_schwarz.c) and applies W = 1/count
+// ascending-element order, oracle_schwarz.c) and applies W = 1/count.  The
+// result sv is stored (u.kind 0) or consumed by the Chebyshev update
+// (kind 4: d = c1 d + c2 sv; kind 1: r -= sv, d = c1 d + c2 r).
+__device__ __forceinline__ void asm_emit(const AsmUpdate& u, double* __restrict__ y, long q, double sv) {
+  if (u.kind == 0) {
+    y[q] = sv;
+  } else if (u.kind == 4) {
+    u.d[q] = u.c1 * u.d[q] + u.c2 * sv;
+  } else {
+    const double rv = u.r[q] - sv;
+    u.r[q] = rv;
+    u.d[q] = u.c1 * u.d[q] + u.c2 * rv;
+  }
+}
+
 template <int N>
-__global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
+__global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y, AsmUpdate u) {
   constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, NOS = sem_nos(N);
   const long n = (long)A.Ex * A.Ey * A.Ezl * NOS;
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n; q += (long)gridDim.x * blockDim.x) {
     const long e = q / NOS;
     int a, b, c;
     if (!sem_abc(N, (int)(q - e * NOS), a, b, c)) {
-      y[q] = 0.0;
+      asm_emit(u, y, q, 0.0);
       continue;
     }
     const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
     const int gx = ex * N + a + 1, gy = ey * N + b + 1, gz = ez * N + c + 1;
     if (gx >= N * A.Ex || gy >= N * A.Ey || gz >= N * A.Ez) {
-      y[q] = 0.0;
+      asm_emit(u, y, q, 0.0);
       continue;
     }
     double acc = 0.0;
@@ -438,7 +452,7 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y) {
         }
       }
     }
-    y[q] = acc * (1.0 / (double)cnt);
+    asm_emit(u, y, q, acc * (1.0 / (double)cnt));
   }
 }
 
@@ -518,11 +532,11 @@ void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
   throw Error(EINVAL_, "Schwarz smoother: unsupported order");
 }
 
-void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s) {
+void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s, const AsmUpdate& u) {
   const long n = (long)a.Ex * a.Ey * a.Ezl * sem_nos(a.N);
   unsigned g = (unsigned)std::min<long>((n + 255) / 256, 148 * 16);
 #define X(nn) \
-  if (a.N == nn) { k_asm_gather<nn><<<g, 256, 0, s>>>(a, y); CMG_LAUNCH_CHECK(); return; }
+  if (a.N == nn) { k_asm_gather<nn><<<g, 256, 0, s>>>(a, y, u); CMG_LAUNCH_CHECK(); return; }
   X(2) X(3) X(4) X(5) X(7)
 #undef X
   throw Error(EINVAL_, "Schwarz smoother: unsupported order");

@@ -1074,7 +1074,7 @@ void schwarz_apply(void* vctx, const double* r, double* out) {
 // Chebyshev-Schwarz recurrence updates (chebyshev_smooth_S).  RAS: the
 // 1/multiplicity scaling and the vector update run in the epilogue of the
 // assembly of the local solutions (EPI_SUPD4 / EPI_SUPD1), so S r is never
-// stored.  ASM: S into scratch, then the vector updates.
+// stored.  ASM: the same updates applied where the box solutions are summed.
 void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2, double* d, double* r) {
   auto* sc = static_cast<cmg_pmg::Schwarz*>(vctx);
   cmg_pmg* p = sc->p;
@@ -1096,14 +1096,14 @@ void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2
     L->run(SEM_LVEC, kind == 4 ? EPI_SUPD4 : EPI_SUPD1, b);
     return;
   }
-  double* sv = p->ctx->workspace(7, L->len);
-  schwarz_apply(vctx, in, sv);
-  if (kind == 4) {
-    launch_lincomb(L->len, c1, d, c2, sv, d, s);
-  } else {
-    launch_axpy(L->len, -1.0, sv, r, s);
-    launch_lincomb(L->len, c1, d, c2, r, d, s);
-  }
+  const SchwarzArgs a = schwarz_local(sc, in);
+  AsmUpdate u;
+  u.kind = kind;
+  u.c1 = c1;
+  u.c2 = c2;
+  u.d = d;
+  u.r = r;
+  sem_asm_gather(a, nullptr, s, u);
 }
 
 void pmg_smooth(cmg_pmg* p, int l, const cmg_cheb_config& cfg, std::size_t order, const double* b,

@@ -172,7 +172,15 @@ struct SchwarzArgs {
 };
 void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s);
 // ASM: y = W sum_e R_e^T Lout_e  (W = 1/number of covering subdomains)
-void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s);
+// optional fused Chebyshev update of the ASM result sv (kind 0: y = sv;
+// 4: d = c1 d + c2 sv; 1: r -= sv, d = c1 d + c2 r)
+struct AsmUpdate {
+  int kind = 0;
+  double c1 = 0, c2 = 0;
+  double* d = nullptr;
+  double* r = nullptr;
+};
+void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s, const AsmUpdate& u = AsmUpdate{});
 // pack the faces the neighbouring slabs need: r planes (what = 0) before the
 // local solves, ASM Lout planes (what = 1) after them
 void sem_schwarz_pack(const SchwarzArgs& a, int what, double* up, double* dn, cudaStream_t s);
