@@ -30,8 +30,9 @@ def main():
     ctx = cm.Context(0)
     rows = []
 
-    def run(tag, P, fam, kpre, kpost):
-        cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
+    def run(tag, P, fam, kpre, kpost, lmin=0.1):
+        cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0], lambda_min_multiplier=lmin),
+                             kpre, kpost)
         M = P.preconditioner(cyc)
         b = P.A.rhs()
         opts = cm.SolveOptions(tol=1e-8, restart=30, maxit=500)
@@ -44,7 +45,7 @@ def main():
         torch.cuda.synchronize()
         r = {"config": tag, "family": cm.Family(fam).name, "cycle": f"({kpre},{kpost})",
              "iterations": rep.iterations, "fine_matvecs": rep.fine_matvecs, "converged": rep.converged,
-             "tts_ms": round(e0.elapsed_time(e1), 3), "rho": rep.rho}
+             "tts_ms": round(e0.elapsed_time(e1), 3), "rho": rep.rho, "lambda_min_multiplier": lmin}
         rows.append(r)
         print(json.dumps(r), flush=True)
 
@@ -91,6 +92,15 @@ def main():
             for fam, kpre, kpost, note in cases:
                 run(f"paper Kershaw eps={eps} E=36^3 (7,3,1) RAS" + (f" [{note}]" if note else ""), P, fam, kpre,
                     kpost)
+            del P
+    if "paper-ras-tune" in only:
+        # the paper's 1st-kind rows use an empirically tuned lambda_min:
+        # scan the multiplier like harness.hpp:172-225 does for the FD problem
+        for eps, k in ((1.0, 2), (0.3, 5)):
+            P = sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 36, geometry=sem.KERSHAW, eps=eps), (7, 3, 1),
+                                 smoother=sem.RAS, ctx=ctx)
+            for lmin in (0.02, 0.05, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6):
+                run(f"paper Kershaw eps={eps} E=36^3 (7,3,1) RAS 1st kind lambda_min scan", P, 0, k, k, lmin)
             del P
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as fh:
