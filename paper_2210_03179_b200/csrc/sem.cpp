@@ -55,6 +55,14 @@ const StreamMemOps& memops() {
   return ops;
 }
 bool stream_mem_ops() { return memops().wait && memops().write; }
+// exchanges smaller than this many doubles stay on NCCL (CMG_PEER_MIN)
+std::size_t peer_min_doubles() {
+  static const std::size_t v = [] {
+    const char* env = std::getenv("CMG_PEER_MIN");
+    return env ? static_cast<std::size_t>(std::atol(env)) : static_cast<std::size_t>(32768);
+  }();
+  return v;
+}
 // the stream waits until *flag >= v (v counts up)
 void stream_wait(cudaStream_t s, const unsigned* flag, unsigned v) {
   if (memops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), v,
@@ -67,6 +75,121 @@ void stream_write(cudaStream_t s, unsigned* flag, unsigned v) {
                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
     fail(CMG_ERUNTIME, "sem: cuStreamWriteValue32 failed");
 }
+
+// Two-way neighbour exchange over peer memory (the pattern of SemLevel's face
+// halo, for the Schwarz ghost planes): every rank packs the part its upper
+// neighbour needs and the part its lower neighbour needs into one IPC-exported,
+// double-buffered buffer; consumers read them through NVLink after a
+// stream-ordered "ready" flag and acknowledge so the producer may reuse the
+// buffer two exchanges later.  Collective setup; all ranks fall back to NCCL
+// together if any mapping fails.
+struct PeerShift {
+  bool on = false;
+  std::size_t nu = 0, nd = 0;
+  DBuf buf;                        // local [2][nu + nd]
+  unsigned* flags = nullptr;       // local: ready from below, ready from above, ack from above, ack from below
+  const double* buf_dn = nullptr;  // rank below's buf (mapped)
+  const double* buf_up = nullptr;  // rank above's buf (mapped)
+  unsigned* flags_dn = nullptr;
+  unsigned* flags_up = nullptr;
+  std::vector<void*> opened;
+  unsigned epoch = 0;
+  int up = -1, down = -1;
+  PeerShift() = default;
+  PeerShift(const PeerShift&) = delete;
+  PeerShift& operator=(const PeerShift&) = delete;
+  ~PeerShift() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    if (flags) cudaFree(flags);
+  }
+
+  void setup(cmg_ctx* ctx, int rank, int nranks, std::size_t n_up, std::size_t n_dn) {
+    const char* env = std::getenv("CMG_PEER_HALO");
+    if (nranks < 2 || (env && std::atoi(env) == 0) || !stream_mem_ops()) return;
+    if (n_up + n_dn < peer_min_doubles()) return;  // same decision on every rank
+    cudaStream_t s = ctx->stream;
+    nu = n_up;
+    nd = n_dn;
+    up = rank + 1 < nranks ? rank + 1 : -1;
+    down = rank > 0 ? rank - 1 : -1;
+    buf.alloc(2 * (nu + nd));
+    buf.zero(s);
+    CMG_CUDA(cudaMalloc(&flags, 4 * sizeof(unsigned)));
+    CMG_CUDA(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned), s));
+    constexpr int HB = 2 * sizeof(cudaIpcMemHandle_t);
+    constexpr int HD = (HB + 7) / 8;
+    std::vector<unsigned char> mine(HD * 8, 0);
+    cudaIpcMemHandle_t h[2];
+    CMG_CUDA(cudaIpcGetMemHandle(&h[0], buf.p));
+    CMG_CUDA(cudaIpcGetMemHandle(&h[1], flags));
+    std::memcpy(mine.data(), h, HB);
+    DBuf dmine(HD), dall(static_cast<std::size_t>(HD) * nranks);
+    CMG_CUDA(cudaMemcpyAsync(dmine.p, mine.data(), HD * 8, cudaMemcpyHostToDevice, s));
+    ctx->comm->allgather(dmine.p, dall.p, HD, s);
+    std::vector<unsigned char> all(static_cast<std::size_t>(HD) * 8 * nranks);
+    CMG_CUDA(cudaMemcpyAsync(all.data(), dall.p, all.size(), cudaMemcpyDeviceToHost, s));
+    CMG_CUDA(cudaStreamSynchronize(s));
+    bool ok = true;
+    auto open = [&](int r, int which) -> void* {
+      cudaIpcMemHandle_t hh;
+      std::memcpy(&hh, all.data() + static_cast<std::size_t>(r) * HD * 8 + which * sizeof(cudaIpcMemHandle_t),
+                  sizeof(hh));
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, hh, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+        return nullptr;
+      }
+      opened.push_back(p);
+      return p;
+    };
+    if (down >= 0) {
+      buf_dn = static_cast<const double*>(open(down, 0));
+      flags_dn = static_cast<unsigned*>(open(down, 1));
+    }
+    if (up >= 0) {
+      buf_up = static_cast<const double*>(open(up, 0));
+      flags_up = static_cast<unsigned*>(open(up, 1));
+    }
+    const double mine_ok = ok ? 1.0 : 0.0;
+    CMG_CUDA(cudaMemcpyAsync(dmine.p, &mine_ok, sizeof(double), cudaMemcpyHostToDevice, s));
+    ctx->comm->allreduce_sum(dmine.p, 1, s);
+    double total = 0.0;
+    CMG_CUDA(cudaMemcpyAsync(&total, dmine.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CMG_CUDA(cudaStreamSynchronize(s));
+    on = total == static_cast<double>(nranks);
+  }
+  // where to pack this exchange's up-going and down-going parts (waits until
+  // both consumers are done with the buffer from two exchanges ago)
+  double* begin(cudaStream_t s) {
+    const unsigned k = ++epoch;
+    if (k > 2) {
+      if (up >= 0) stream_wait(s, flags + 2, k - 2);
+      if (down >= 0) stream_wait(s, flags + 3, k - 2);
+    }
+    return buf.p + (k & 1) * (nu + nd);
+  }
+  // after the pack: publish it, wait for the neighbours' packs, return their parts
+  void post(cudaStream_t s, const double** lo, const double** hi) {
+    const unsigned k = epoch;
+    if (up >= 0) stream_write(s, flags_up + 0, k);
+    if (down >= 0) stream_write(s, flags_dn + 1, k);
+    if (down >= 0) {
+      stream_wait(s, flags + 0, k);
+      *lo = buf_dn + (k & 1) * (nu + nd);
+    }
+    if (up >= 0) {
+      stream_wait(s, flags + 1, k);
+      *hi = buf_up + (k & 1) * (nu + nd) + nu;
+    }
+  }
+  // after the kernel that read the neighbours' parts
+  void done(cudaStream_t s) {
+    const unsigned k = epoch;
+    if (down >= 0) stream_write(s, flags_dn + 2, k);
+    if (up >= 0) stream_write(s, flags_up + 3, k);
+  }
+};
 
 template <class F>
 int guard(F&& f) {
@@ -355,6 +478,7 @@ struct SemLevel final : cmg_op {
   void peer_setup() {
     const char* env = std::getenv("CMG_PEER_HALO");
     if (!distributed() || (env && std::atoi(env) == 0) || !stream_mem_ops()) return;
+    if (static_cast<std::size_t>(Ex) * Ey * N * N < peer_min_doubles()) return;  // small levels: NCCL
     cudaStream_t s = ctx->stream;
     peer.hn = static_cast<std::size_t>(Ex) * Ey * N * N;
     peer.cn = static_cast<std::size_t>(Ex) * Ey * (N + 1) * (N + 1);
@@ -669,7 +793,8 @@ struct cmg_pmg {
   // Schwarz smoother data per smoothed level
   struct Schwarz {
     DBuf S, lam, Lout, wmult;
-    DBuf rsend, rlo, rhi, Lsend, Llo, Lhi;  // slab faces (partitioned levels)
+    DBuf rsend, rlo, rhi, Lsend, Llo, Lhi;  // slab faces (partitioned levels, NCCL path)
+    PeerShift rpeer, Lpeer;                 // the same faces through peer memory (default)
     IBuf sidx;
     cmg_pmg* p = nullptr;
     int level = 0;
@@ -993,6 +1118,7 @@ void schwarz_setup(cmg_pmg* p, int l) {
     sc->rhi.alloc(rd);
     sc->rlo.zero(p->ctx->stream);
     sc->rhi.zero(p->ctx->stream);
+    sc->rpeer.setup(p->ctx, L->desc.rank, L->desc.nranks, ru, rd);
     if (!ras) {
       const long lu = schwarz_ghost_up(g, 1), ld = schwarz_ghost_dn(g, 1);
       sc->Lsend.alloc(lu + ld);
@@ -1000,6 +1126,7 @@ void schwarz_setup(cmg_pmg* p, int l) {
       sc->Lhi.alloc(ld);
       sc->Llo.zero(p->ctx->stream);
       sc->Lhi.zero(p->ctx->stream);
+      sc->Lpeer.setup(p->ctx, L->desc.rank, L->desc.nranks, lu, ld);
     }
   }
   if (static_cast<int>(p->sch.size()) <= l) p->sch.resize(l + 1);
@@ -1035,22 +1162,40 @@ SchwarzArgs schwarz_local(cmg_pmg::Schwarz* sc, const double* r) {
   a.Lout = sc->Lout.p;
   a.ras = p->smoother == 2;
   const bool part = L->distributed();
-  if (part) {  // r planes of the neighbouring slabs (NCCL, one group)
+  if (part) {  // r planes of the neighbouring slabs
     const long ru = schwarz_ghost_up(a, 0), rd = schwarz_ghost_dn(a, 0);
-    sem_schwarz_pack(a, 0, sc->rsend.p, sc->rsend.p + ru, s);
-    p->ctx->comm->shift(sc->rsend.p, sc->rlo.p, ru, sc->rsend.p + ru, sc->rhi.p, rd, L->up(), L->down(), s);
-    a.rlo = sc->rlo.p;
-    a.rhi = sc->rhi.p;
+    if (sc->rpeer.on) {  // read in place from the neighbours' pack buffers (NVLink)
+      double* send = sc->rpeer.begin(s);
+      sem_schwarz_pack(a, 0, send, send + ru, s);
+      sc->rpeer.post(s, &a.rlo, &a.rhi);
+    } else {  // NCCL, one group
+      sem_schwarz_pack(a, 0, sc->rsend.p, sc->rsend.p + ru, s);
+      p->ctx->comm->shift(sc->rsend.p, sc->rlo.p, ru, sc->rsend.p + ru, sc->rhi.p, rd, L->up(), L->down(), s);
+      a.rlo = sc->rlo.p;
+      a.rhi = sc->rhi.p;
+    }
   }
   sem_schwarz_local(a, s);
+  if (part && sc->rpeer.on) sc->rpeer.done(s);
   if (part && !a.ras) {  // ASM also sums the neighbouring layers' boxes
     const long lu = schwarz_ghost_up(a, 1), ld = schwarz_ghost_dn(a, 1);
-    sem_schwarz_pack(a, 1, sc->Lsend.p, sc->Lsend.p + lu, s);
-    p->ctx->comm->shift(sc->Lsend.p, sc->Llo.p, lu, sc->Lsend.p + lu, sc->Lhi.p, ld, L->up(), L->down(), s);
-    a.Llo = sc->Llo.p;
-    a.Lhi = sc->Lhi.p;
+    if (sc->Lpeer.on) {  // released by asm_done() after the gather
+      double* send = sc->Lpeer.begin(s);
+      sem_schwarz_pack(a, 1, send, send + lu, s);
+      sc->Lpeer.post(s, &a.Llo, &a.Lhi);
+    } else {
+      sem_schwarz_pack(a, 1, sc->Lsend.p, sc->Lsend.p + lu, s);
+      p->ctx->comm->shift(sc->Lsend.p, sc->Llo.p, lu, sc->Lsend.p + lu, sc->Lhi.p, ld, L->up(), L->down(), s);
+      a.Llo = sc->Llo.p;
+      a.Lhi = sc->Lhi.p;
+    }
   }
   return a;
+}
+
+// after the ASM gather that read the neighbours' box planes
+void asm_done(cmg_pmg::Schwarz* sc) {
+  if (sc->Lpeer.on) sc->Lpeer.done(sc->p->ctx->stream);
 }
 
 // out = S_ASM r or S_RAS r on level l
@@ -1068,6 +1213,7 @@ void schwarz_apply(void* vctx, const double* r, double* out) {
     launch_mul(L->len, sc->wmult.p, out, s);
   } else {
     sem_asm_gather(a, out, s);
+    asm_done(sc);
   }
 }
 
@@ -1104,6 +1250,7 @@ void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2
   u.d = d;
   u.r = r;
   sem_asm_gather(a, nullptr, s, u);
+  asm_done(sc);
 }
 
 void pmg_smooth(cmg_pmg* p, int l, const cmg_cheb_config& cfg, std::size_t order, const double* b,
@@ -1313,6 +1460,11 @@ int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const in
         p->lambda[l] = estimate_lambda_max_S(p->lev[l].get(), schwarz_apply, p->sch[l].get(), eigen_iterations,
                                              eigen_seed);
       }
+      // a non-positive Rayleigh quotient means an indefinite level operator, e.g.
+      // a Kershaw map whose kinks (y, z = 1/2) fall inside elements at small eps
+      if (!(p->lambda[l] > 0.0))
+        fail(CMG_EINVAL, "pmg: level " + std::to_string(l) +
+                             " operator is not positive definite (deformed mesh invalid at this resolution?)");
       p->lev[l]->count = 0;
     }
     ctx->sync();

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--kpost", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--eps", type=float, default=0.0, help="Kershaw deformation (0: undeformed box)")
+    ap.add_argument("--ez", type=int, default=0, help="element layers (default E)")
     args = ap.parse_args()
     import torch
 
@@ -47,7 +48,7 @@ def main():
         ctx.attach_nccl(uid[0], rank, world)
     E = args.E
     geo = dict(geometry=sem.KERSHAW, eps=args.eps) if args.eps > 0 else {}
-    d = sem.SemDesc(7, E, E, E, rank=rank, nranks=world, **geo)
+    d = sem.SemDesc(7, E, E, args.ez or E, rank=rank, nranks=world, **geo)
     P = sem.PMGHierarchy(d, (7, 3, 1), smoother=args.smoother, ctx=ctx)
     stream = torch.cuda.current_stream()
 
@@ -90,7 +91,7 @@ def main():
     barrier()
     tts_ms = max_ms(e0.elapsed_time(e1))
     if rank == 0:
-        print(json.dumps({"tool": "schwarz_scaling", "n_gpus": world, "E": E, "N": 7,
+        print(json.dumps({"tool": "schwarz_scaling", "n_gpus": world, "E": E, "ez": args.ez or E, "N": 7,
                           "unknowns": d.unknowns(), "kershaw_eps": args.eps or None, "smoother": {1: "ASM", 2: "RAS"}[args.smoother],
                           "family": cm.Family(args.family).name, "cycle": f"({args.kpre},{args.kpost})",
                           "sweep_ms": sweep_ms, "iterations": rep.iterations, "fine_matvecs": rep.fine_matvecs,
