@@ -124,6 +124,14 @@ def test_pmg_solves_match_reference_templates(cm, sem, fam, kpre, kpost, driver)
     assert np.linalg.norm(P.A.to_canonical(x) - oref.x) <= TOL * np.linalg.norm(oref.x)
 
 
+def test_indefinite_level_rejected(sem):
+    """A Kershaw eps=0.05 map whose z-kink (z = 1/2) falls inside an element
+    layer (ez = 9) gives an indefinite interpolated geometry: setup refuses it
+    with EINVAL instead of smoothing with a negative lambda_tilde."""
+    with pytest.raises(ValueError, match="not positive definite"):
+        sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 9, geometry=sem.KERSHAW, eps=0.05), (7, 3, 1))
+
+
 @pytest.mark.parametrize("eps,kpre,kpost,htol", [(0.3, 4, 0, TOL), (0.3, 8, 0, TOL), (0.5, 4, 0, TOL),
                                                  (0.5, 2, 2, TOL), (0.3, 2, 2, 1e-6)])
 def test_kershaw_solves(cm, sem, eps, kpre, kpost, htol):
