@@ -238,7 +238,7 @@ void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& 
         A->cheb4_step(bi, 1.0, 0.0, xz, d, r, x, r, d, d2, 0.0);
         d = d2;
         xz = false;
-        U(sctx, 4, r, c1, c2, d, r);
+        U(sctx, 4, r, c1, c2, d, r, nullptr, 0);
         continue;
       }
       if (xz) launch_scal_copy(L, nullptr, bi, d, x, s);
@@ -259,18 +259,21 @@ void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& 
     CMG_CUDA(cudaMemcpyAsync(r, sv, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
     launch_scal_copy(L, nullptr, 1.0 / theta, r, d, s);
     for (std::size_t it = 1; it < order; ++it) {
+      const double rho = 1.0 / (2.0 * sigma - rho_prev);
+      if (U) {  // x += d joins the S update (it reads d at the same slot)
+        A->apply(d, t);
+        U(sctx, 1, t, rho * rho_prev, 2.0 * rho / delta, d, r, x, xz ? 1 : 0);
+        xz = false;
+        rho_prev = rho;
+        continue;
+      }
       if (xz) CMG_CUDA(cudaMemcpyAsync(x, d, L * sizeof(double), cudaMemcpyDeviceToDevice, s));
       else launch_axpy(L, 1.0, d, x, s);
       xz = false;
       A->apply(d, t);
-      const double rho = 1.0 / (2.0 * sigma - rho_prev);
-      if (U) {
-        U(sctx, 1, t, rho * rho_prev, 2.0 * rho / delta, d, r);
-      } else {
-        S(sctx, t, sv);
-        launch_axpy(L, -1.0, sv, r, s);
-        launch_lincomb(L, rho * rho_prev, d, 2.0 * rho / delta, r, d, s);
-      }
+      S(sctx, t, sv);
+      launch_axpy(L, -1.0, sv, r, s);
+      launch_lincomb(L, rho * rho_prev, d, 2.0 * rho / delta, r, d, s);
       rho_prev = rho;
     }
     vec_final_update(L, 1.0, xz, d, x, s);

@@ -220,8 +220,10 @@ void host_fdm_1d(int N, const double* w, const double* D, double Ll, double L, d
 // (S(in, out): out = S in) -- the Schwarz path
 using SApply = void (*)(void* ctx, const double* in, double* out);
 // optional fused recurrence update (same arithmetic as S followed by the
-// vector updates):  kind 4: d = c1 d + c2 S in ;  kind 1: r -= S in, d = c1 d + c2 r
-using SUpdate = void (*)(void* ctx, int kind, const double* in, double c1, double c2, double* d, double* r);
+// vector updates):  kind 4: d = c1 d + c2 S in ;  kind 1: x += d (x = d if x_zero),
+// r -= S in, d = c1 d + c2 r
+using SUpdate = void (*)(void* ctx, int kind, const double* in, double c1, double c2, double* d, double* r,
+                         double* x, int x_zero);
 void chebyshev_smooth_S(cmg_op* A, SApply S, void* sctx, const cmg_cheb_config& cfg, std::size_t order,
                         const double* b, double* x, bool x_is_zero, SUpdate U = nullptr);
 double estimate_lambda_max_S(cmg_op* A, SApply S, void* sctx, std::size_t iterations, std::uint64_t seed);

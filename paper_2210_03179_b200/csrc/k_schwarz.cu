@@ -411,6 +411,7 @@ __device__ __forceinline__ void asm_emit(const AsmUpdate& u, double* __restrict_
   } else if (u.kind == 4) {
     u.d[q] = u.c1 * u.d[q] + u.c2 * sv;
   } else {
+    if (u.x) u.x[q] = u.x_zero ? u.d[q] : u.x[q] + u.d[q];
     const double rv = u.r[q] - sv;
     u.r[q] = rv;
     u.d[q] = u.c1 * u.d[q] + u.c2 * rv;

@@ -142,6 +142,7 @@ __device__ __forceinline__ void epilogue(const SemArgs& A, long slot, double w, 
   } else if constexpr (EPI == EPI_SUPD4) {
     A.d_out[slot] = A.c1 * o1 + A.c2 * (o0 * w);
   } else if constexpr (EPI == EPI_SUPD1) {
+    if (A.x) A.x[slot] = A.x_zero ? o2 : A.x[slot] + o2;  // x += d (the pre-update d)
     const double rv = o0 - o1 * w;
     A.r[slot] = rv;
     A.d_out[slot] = A.c1 * o2 + A.c2 * rv;

@@ -1221,7 +1221,8 @@ void schwarz_apply(void* vctx, const double* r, double* out) {
 // 1/multiplicity scaling and the vector update run in the epilogue of the
 // assembly of the local solutions (EPI_SUPD4 / EPI_SUPD1), so S r is never
 // stored.  ASM: the same updates applied where the box solutions are summed.
-void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2, double* d, double* r) {
+void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2, double* d, double* r, double* x,
+                    int x_zero) {
   auto* sc = static_cast<cmg_pmg::Schwarz*>(vctx);
   cmg_pmg* p = sc->p;
   SemLevel* L = p->lev[sc->level].get();
@@ -1238,6 +1239,8 @@ void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2
     if (kind == 1) {
       b.r_in = r;
       b.r = r;
+      b.x = x;
+      b.x_zero = x_zero;
     }
     L->run(SEM_LVEC, kind == 4 ? EPI_SUPD4 : EPI_SUPD1, b);
     return;
@@ -1249,6 +1252,8 @@ void schwarz_update(void* vctx, int kind, const double* in, double c1, double c2
   u.c2 = c2;
   u.d = d;
   u.r = r;
+  u.x = x;
+  u.x_zero = x_zero;
   sem_asm_gather(a, nullptr, s, u);
   asm_done(sc);
 }

@@ -33,7 +33,7 @@ enum SemEpi : int {
   // Chebyshev-Schwarz (RAS) updates fused into the assembly of the local
   // solutions (L-vector mode), invd = 1/multiplicity:
   EPI_SUPD4 = 7,      // d_out = c1 d + c2 (invd w)             (4th kind: d = c1 d + c2 S r)
-  EPI_SUPD1 = 8       // r = r_in - invd w ; d_out = c1 d + c2 r (1st kind: r -= S t; d = c1 d + c2 r)
+  EPI_SUPD1 = 8       // [x += d] ; r = r_in - invd w ; d_out = c1 d + c2 r (1st kind: r -= S t; d = c1 d + c2 r)
 };
 
 // K2 contributor table row: [count | a<<8 | b<<16 | c<<24], then per contribution
@@ -179,6 +179,8 @@ struct AsmUpdate {
   double c1 = 0, c2 = 0;
   double* d = nullptr;
   double* r = nullptr;
+  double* x = nullptr;  // kind 1: x += d first (x = d if x_zero)
+  int x_zero = 0;
 };
 void sem_asm_gather(const SchwarzArgs& a, double* y, cudaStream_t s, const AsmUpdate& u = AsmUpdate{});
 // pack the faces the neighbouring slabs need: r planes (what = 0) before the
