@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--eps", type=float, default=0.0, help="Kershaw deformation (0: undeformed box)")
     ap.add_argument("--ez", type=int, default=0, help="element layers (default E)")
+    ap.add_argument("--lmin", type=float, default=0.1, help="lambda_min multiplier (1st kind)")
     args = ap.parse_args()
     import torch
 
@@ -67,7 +68,7 @@ def main():
 
     b = P.A.rhs()
     # one fine-level Chebyshev-Schwarz sweep of order kpre (the (kpre,0) half cycle's smoother)
-    ccfg = cm.ChebyshevConfig(cm.Family(args.family), args.kpre, P.lambda_tilde[0])
+    ccfg = cm.ChebyshevConfig(cm.Family(args.family), args.kpre, P.lambda_tilde[0], lambda_min_multiplier=args.lmin)
     x = P.A.new_vector()
     for _ in range(3):
         P.smooth(0, ccfg, args.kpre, b, x, True)
@@ -80,7 +81,8 @@ def main():
     barrier()
     sweep_ms = max_ms(e0.elapsed_time(e1) / args.reps)
 
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(args.family), 1, P.lambda_tilde[0]), args.kpre, args.kpost)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(args.family), 1, P.lambda_tilde[0],
+                                            lambda_min_multiplier=args.lmin), args.kpre, args.kpost)
     M = P.preconditioner(cyc)
     opts = cm.SolveOptions(tol=1e-8, restart=30, maxit=500)
     cm.pgmres(P.A, M, b, None, opts)
@@ -93,7 +95,7 @@ def main():
     if rank == 0:
         print(json.dumps({"tool": "schwarz_scaling", "n_gpus": world, "E": E, "ez": args.ez or E, "N": 7,
                           "unknowns": d.unknowns(), "kershaw_eps": args.eps or None, "smoother": {1: "ASM", 2: "RAS"}[args.smoother],
-                          "family": cm.Family(args.family).name, "cycle": f"({args.kpre},{args.kpost})",
+                          "family": cm.Family(args.family).name, "cycle": f"({args.kpre},{args.kpost})", "lambda_min_multiplier": args.lmin,
                           "sweep_ms": sweep_ms, "iterations": rep.iterations, "fine_matvecs": rep.fine_matvecs,
                           "converged": rep.converged, "time_to_solution_s": tts_ms * 1e-3,
                           "ms_per_iteration": tts_ms / max(rep.iterations, 1)}), flush=True)
