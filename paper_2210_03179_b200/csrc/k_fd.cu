@@ -202,10 +202,12 @@ __global__ void k_fd_prolong(int mf, int mc, int f, const double* __restrict__ e
 // Strided small-GEMM "mode product": contract dimension `dim` of a 3D array.
 // out[o, r] = sum_m Mop(o, m) in[m, r]; Mop = M (row-major, ld) or M^T.
 // 16x16 output tile per 256-thread block (one output per thread, 64 blocks at
-// the n=256 coarse grid), k in tiles of 64 accumulated in ascending order.
+// the n=256 coarse grid), k in tiles of 128 accumulated in ascending order
+// (one staging round for every coarse grid up to 128: the launch is latency
+// bound, not bandwidth bound, so the second load/sync round was pure cost).
 // Loads and stores walk whichever of (k, r) is unit-stride so both stay
 // coalesced for every contracted dimension.
-constexpr int TM = 16, TR = 16, TK = 64;
+constexpr int TM = 16, TR = 16, TK = 128;
 __global__ void __launch_bounds__(256) k_mode_product(int nd, int na, int nb, long sd, long sa, long sb,
                                                       const double* __restrict__ M, int ld, int transpose,
                                                       const double* __restrict__ in, double* __restrict__ out,
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(256) k_mode_product(int nd, int na, int nb, lo
     }
     __syncthreads();
     const int kn = min(TK, nd - k0);
+#pragma unroll 8
     for (int kk = 0; kk < kn; ++kk) acc += Ms[oo][kk] * Bs[kk][ro];
     __syncthreads();
   }
