@@ -202,12 +202,12 @@ __global__ void k_fd_prolong(int mf, int mc, int f, const double* __restrict__ e
 // Strided small-GEMM "mode product": contract dimension `dim` of a 3D array.
 // out[o, r] = sum_m Mop(o, m) in[m, r]; Mop = M (row-major, ld) or M^T.
 // 16x16 output tile per 256-thread block (one output per thread, 64 blocks at
-// the n=256 coarse grid), k in tiles of 128 accumulated in ascending order
-// (one staging round for every coarse grid up to 128: the launch is latency
-// bound, not bandwidth bound, so the second load/sync round was pure cost).
+// the n=256 coarse grid), k in tiles of TK (64 or 128, one staging round for
+// every coarse grid up to 128) accumulated in ascending order.
 // Loads and stores walk whichever of (k, r) is unit-stride so both stay
 // coalesced for every contracted dimension.
-constexpr int TM = 16, TR = 16, TK = 128;
+constexpr int TM = 16, TR = 16;
+template <int TK>
 __global__ void __launch_bounds__(256) k_mode_product(int nd, int na, int nb, long sd, long sa, long sb,
                                                       const double* __restrict__ M, int ld, int transpose,
                                                       const double* __restrict__ in, double* __restrict__ out,
@@ -221,22 +221,34 @@ __global__ void __launch_bounds__(256) k_mode_product(int nd, int na, int nb, lo
   const int oo = kfast ? t % TM : t / TR, ro = kfast ? t / TM : t % TR;
   double acc = 0.0;
   for (int k0 = 0; k0 < nd; k0 += TK) {
-    for (int e = t; e < TM * TK; e += 256) {
+    // All global loads of the stage are issued before any shared store: the
+    // launch is load-latency bound (one dependent load->store pair per
+    // element serialised ~16 DRAM round trips).
+    constexpr int LM = TM * TK / 256, LB = TK * TR / 256;
+    double vm[LM], vb[LB];
+#pragma unroll
+    for (int i = 0; i < LM; ++i) {
+      const int e = t + i * 256;
       const int mo = transpose ? e % TM : e / TK, mk = transpose ? e / TM : e % TK;
       const int o = o0 + mo, k = k0 + mk;
-      double v = 0.0;
-      if (o < nd && k < nd) v = transpose ? M[(long)k * ld + o] : M[(long)o * ld + k];
-      Ms[mo][mk] = v;
+      vm[i] = (o < nd && k < nd) ? (transpose ? M[(long)k * ld + o] : M[(long)o * ld + k]) : 0.0;
     }
-    for (int e = t; e < TK * TR; e += 256) {
+#pragma unroll
+    for (int i = 0; i < LB; ++i) {
+      const int e = t + i * 256;
       const int kk = kfast ? e % TK : e / TR, rr = kfast ? e / TK : e % TR;
       const int k = k0 + kk, r = r0 + rr;
-      double v = 0.0;
-      if (k < nd && r < R) {
-        const int ra = r % na, rb = r / na;
-        v = in[(long)k * sd + (long)ra * sa + (long)rb * sb];
-      }
-      Bs[kk][rr] = v;
+      vb[i] = (k < nd && r < R) ? in[(long)k * sd + (long)(r % na) * sa + (long)(r / na) * sb] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < LM; ++i) {
+      const int e = t + i * 256;
+      Ms[transpose ? e % TM : e / TK][transpose ? e / TM : e % TK] = vm[i];
+    }
+#pragma unroll
+    for (int i = 0; i < LB; ++i) {
+      const int e = t + i * 256;
+      Bs[kfast ? e % TK : e / TR][kfast ? e / TK : e % TR] = vb[i];
     }
     __syncthreads();
     const int kn = min(TK, nd - k0);
@@ -332,8 +344,12 @@ void mode_product_s0(int dim, int n0, int n1, int n2, long s0, long s1, long s2,
   const int nd = n[dim];
   const int R = n[a] * n[b];
   dim3 grid((R + TR - 1) / TR, (nd + TM - 1) / TM);
-  k_mode_product<<<grid, 256, 0, s>>>(nd, n[a], n[b], st[dim], st[a], st[b], M, ld, transpose, in,
-                                       out, div);
+  if (nd <= 64)  // the SEM p=1 boxes: half the staging footprint, more resident blocks
+    k_mode_product<64><<<grid, 256, 0, s>>>(nd, n[a], n[b], st[dim], st[a], st[b], M, ld, transpose,
+                                            in, out, div);
+  else
+    k_mode_product<128><<<grid, 256, 0, s>>>(nd, n[a], n[b], st[dim], st[a], st[b], M, ld, transpose,
+                                             in, out, div);
   CMG_LAUNCH_CHECK();
 }
 
