@@ -861,25 +861,31 @@ __global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double*
 // ---------------------------------------------------------------- layer dots
 // partials[(v*L + layer)*LCH + chunk]
 constexpr int LCH = 16;
+// MAXC: 8 in general, 1 for the single dots (norms, <v, w>): one accumulator
+// leaves the registers to unroll the stride loop so several loads are in
+// flight per thread. Either way each accumulator sums its terms in ascending
+// q and the block reduction is the same, so the partials keep their bits.
+template <int MAXC>
 __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int nv,
                              const double* __restrict__ w, long layer_len, int nlayers,
                              double* __restrict__ partials) {
   const int layer = blockIdx.y, chunk = blockIdx.x, v0 = blockIdx.z * 8;
   const int cnt = min(8, nv - v0);
-  __shared__ double sh[8][8];
-  double acc[8];
+  __shared__ double sh[MAXC][8];
+  double acc[MAXC];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
   const long base = (long)layer * layer_len;
+#pragma unroll(MAXC == 1 ? 4 : 1)
   for (long q = (long)chunk * blockDim.x + threadIdx.x; q < layer_len; q += (long)LCH * blockDim.x) {
     const double wv = w[base + q];
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
+    for (int c = 0; c < MAXC; ++c)
       if (c < cnt) acc[c] += V[(std::size_t)(v0 + c) * ldv + base + q] * wv;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
+  for (int c = 0; c < MAXC; ++c) {
     double v = acc[c];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -1095,7 +1101,10 @@ void sem_restrict_local(const SemArgs& f, int Nc, const double* J, const double*
 void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
                     int nlayers, double* partials, double* out, cudaStream_t s) {
   dim3 grid(LCH, nlayers, (nv + 7) / 8);
-  k_layer_dots<<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+  if (nv == 1)
+    k_layer_dots<1><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+  else
+    k_layer_dots<8><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
   CMG_LAUNCH_CHECK();
   const long t = (long)nv * nlayers;
   k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
