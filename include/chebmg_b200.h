@@ -192,6 +192,14 @@ int cmg_sem_gs_map_host(const cmg_sem_desc* desc, int64_t* map_host);
 size_t cmg_sem_local_slots(const cmg_sem_desc* desc);
 /* RHS b = Q^T B f into a device slot vector */
 int cmg_sem_rhs(cmg_op* op, double* b);
+/* host tables the device operators are built from: GLL
+ * nodes xi[N+1], weights w[N+1], derivative matrix D[(N+1)^2] (row-major,
+ * D[i*(N+1)+j] = l_j'(xi_i)); interpolation J[(Nf+1)*(Nc+1)]; the 1D Schwarz
+ * FDM basis S[(N+3)^2] / lam[N+3] of an extended element.  No device needed. */
+int cmg_sem_basis_host(int N, double* xi, double* w, double* D);
+int cmg_sem_interp_host(int Nf, int Nc, double* J);
+int cmg_sem_fdm1d_host(int N, double Ll, double L, double Lr, int dl, int d0, int dN, int dr, double* S,
+                       double* lam);
 
 /* p-multigrid hierarchy: orders e.g. {7,3,1}; smoother 0 Chebyshev-Jacobi, 1 ASM, 2 RAS */
 int cmg_pmg_create(cmg_ctx* ctx, const cmg_sem_desc* fine, int nlevels, const int* orders,

@@ -187,6 +187,11 @@ typedef struct orc_pmg orc_pmg;
 /* smoother: 0 Jacobi, 1 ASM, 2 RAS */
 orc_pmg* orc_pmg_create(int nlevels, const int* orders, int Ex, int Ey, int Ez, int geometry,
                         double eps, int smoother, size_t eigen_iterations, uint64_t eigen_seed);
+enum { ORC_PMG_NO_LAMBDA = 1, ORC_PMG_NO_COARSE = 2 };
+orc_pmg* orc_pmg_create_ex(int nlevels, const int* orders, int Ex, int Ey, int Ez, int geometry,
+                           double eps, int smoother, size_t eigen_iterations, uint64_t eigen_seed,
+                           int flags);
+size_t orc_sem_local_triplets(const orc_sem* s, int64_t* rows, int64_t* cols, double* vals);
 void orc_pmg_destroy(orc_pmg* p);
 orc_op* orc_pmg_op(orc_pmg* p, int level);
 orc_sem* orc_pmg_sem(orc_pmg* p, int level);

@@ -16,7 +16,9 @@
  *    decoupled (identity row/col), which leaves the reduced solve exact.
  *  - FDM: A_* S = B_* S Lambda, S^T B_* S = I, Abar^{-1} =
  *    (Sz x Sy x Sx) D^{-1} (Sz x Sy x Sx)^T, D = I x I x Lx + I x Ly x I + Lz x I x I
- *    (PAPER.md:587-613).
+ *    (PAPER.md:587-613).  Each mode-product output is one fma() chain over
+ *    ascending m -- the rounding of the GPU's k_schwarz_local (__fma_rn), so
+ *    the local solves compare bit for bit.
  *  - ASM: S r = W_asm (sum_e R_e^T Abar_e^{-1} R_e r), W_asm = 1 / (number of
  *    extended subdomains covering the node) -- post-multiplied.
  *  - RAS: S r = W_mult (sum_e Q_e^T [Abar_e^{-1} R_e r restricted to the
@@ -78,11 +80,53 @@ void orc_sym_eig(int n, double* A, double* lam, double* V) {
   for (int i = 0; i < n; ++i) lam[i] = A[i * n + i];
 }
 
+/* A s = lam B s with B SPD: B = L L^T, C = L^{-1} A L^{-T} (symmetrised),
+ * C Q = Q Lambda (cyclic Jacobi), S = L^{-T} Q so that S^T B S = I.  Same
+ * operation sequence as the GPU library's setup (csrc/host_setup.cpp
+ * host_sym_geneig), so the eigenbases -- and with them the local solves --
+ * are bit-identical. */
+static void sym_geneig(int n, const double* A, const double* B, double* S, double* lam) {
+  double L[PB * PB], Li[PB * PB], C[PB * PB], Q[PB * PB];
+  memset(L, 0, sizeof L);
+  memset(Li, 0, sizeof Li);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = B[i * n + j];
+      for (int k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+      if (i == j)
+        L[i * n + i] = sqrt(s);
+      else
+        L[i * n + j] = s / L[j * n + j];
+    }
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i * n + k] * Li[k * n + j];
+      Li[i * n + j] = s / L[i * n + i];
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < n; ++k)
+        for (int l = 0; l < n; ++l) s += Li[i * n + k] * A[k * n + l] * Li[j * n + l];
+      C[i * n + j] = s;
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) C[i * n + j] = C[j * n + i] = 0.5 * (C[i * n + j] + C[j * n + i]);
+  orc_sym_eig(n, C, lam, Q);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < n; ++k) s += Li[k * n + i] * Q[k * n + j];
+      S[i * n + j] = s;
+    }
+}
+
 /* 1D extended operators for one direction.
  * L = element length, Ll/Lr = neighbour lengths (ignored when that side is absent),
  * dl/dr = 1 if the extended node at index 0 / pbar-1 is a global Dirichlet node,
  * d0/dN = 1 if the element's own node 0 / N is a global Dirichlet node.
- * Output: S (pbar x pbar, column eigenvectors) and lam (pbar). */
+ * Output: S (pbar x pbar, column eigenvectors, S^T B S = I) and lam (pbar). */
 void orc_fdm_1d(int N, const double* xi, const double* w, const double* D, double Ll, double L,
                 double Lr, int dl, int d0, int dN, int dr, double* S, double* lam) {
   (void)xi;
@@ -102,31 +146,21 @@ void orc_fdm_1d(int N, const double* xi, const double* w, const double* D, doubl
       }
     }
   }
-  /* restrict to patch indices N-1 .. 2N+1 */
-  double A[PB * PB], B[PB];
-  for (int a = 0; a < pb; ++a) {
-    B[a] = M[N - 1 + a];
-    for (int b = 0; b < pb; ++b) A[a * pb + b] = K[(N - 1 + a) * np + (N - 1 + b)];
-  }
+  /* restrict to patch indices N-1 .. 2N+1; Dirichlet-eliminated nodes decoupled */
   int dirm[PB];
   memset(dirm, 0, sizeof dirm);
   if (dl) dirm[0] = 1;
   if (d0) { dirm[0] = 1; dirm[1] = 1; }
   if (dN) { dirm[pb - 1] = 1; dirm[pb - 2] = 1; }
   if (dr) dirm[pb - 1] = 1;
-  for (int a = 0; a < pb; ++a)
-    if (dirm[a]) {
-      for (int b = 0; b < pb; ++b) A[a * pb + b] = A[b * pb + a] = 0.0;
-      A[a * pb + a] = 1.0;
-      B[a] = 1.0;
-    }
-  /* C = B^{-1/2} A B^{-1/2}; S = B^{-1/2} Q */
-  double C[PB * PB], Q[PB * PB];
-  for (int a = 0; a < pb; ++a)
-    for (int b = 0; b < pb; ++b) C[a * pb + b] = A[a * pb + b] / sqrt(B[a] * B[b]);
-  orc_sym_eig(pb, C, lam, Q);
-  for (int a = 0; a < pb; ++a)
-    for (int b = 0; b < pb; ++b) S[a * pb + b] = Q[a * pb + b] / sqrt(B[a]);
+  double A[PB * PB], B[PB * PB];
+  memset(B, 0, sizeof B);
+  for (int a = 0; a < pb; ++a) {
+    B[a * pb + a] = dirm[a] ? 1.0 : M[N - 1 + a];
+    for (int b = 0; b < pb; ++b)
+      A[a * pb + b] = (dirm[a] || dirm[b]) ? (a == b ? 1.0 : 0.0) : K[(N - 1 + a) * np + (N - 1 + b)];
+  }
+  sym_geneig(pb, A, B, S, lam);
 }
 
 /* element edge-length box approximation */
@@ -216,7 +250,7 @@ void orc_sem_schwarz(const orc_sem* s, int ras, const double* r, double* out) {
             for (int m = 0; m < pb; ++m) {
               const int o = dim == 0 ? a : (dim == 1 ? b : c);
               const int idx = dim == 0 ? m + pb * (b + pb * c) : (dim == 1 ? a + pb * (m + pb * c) : a + pb * (b + pb * m));
-              v += S[m * pb + o] * u[idx];
+              v = fma(S[m * pb + o], u[idx], v);
             }
             t[a + pb * (b + pb * c)] = v;
           }
@@ -234,7 +268,7 @@ void orc_sem_schwarz(const orc_sem* s, int ras, const double* r, double* out) {
             for (int m = 0; m < pb; ++m) {
               const int o = dim == 0 ? a : (dim == 1 ? b : c);
               const int idx = dim == 0 ? m + pb * (b + pb * c) : (dim == 1 ? a + pb * (m + pb * c) : a + pb * (b + pb * m));
-              v += S[o * pb + m] * u[idx];
+              v = fma(S[o * pb + m], u[idx], v);
             }
             t[a + pb * (b + pb * c)] = v;
           }

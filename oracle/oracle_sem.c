@@ -310,7 +310,20 @@ void orc_sem_geom(const orc_sem* s, double* G, double* B) {
   if (B) memcpy(B, s->B, (size_t)s->E * s->np * sizeof(double));
 }
 
-/* ---- A3: local matrix-free operator ---- */
+/* ---- A3: local matrix-free operator ----
+ * Arithmetic contract shared with the GPU kernels (paper_2210_03179_b200/csrc/
+ * k_sem.cu "arithmetic contract"; that file is built with --fmad=false and
+ * places __fma_rn exactly where this file calls fma()), so the two round
+ * identically and the operator is compared bit for bit:
+ *   1D contraction  v = 0; for m ascending: v = fma(D_m, u_m, v)
+ *   geometry        w_a = fma(g_c, u_t, fma(g_b, u_s, g_a * u_r))
+ *   divergence      out = v_t + (v_r + v_s)     (three separate chains)
+ * The summation order is a choice of this restatement (the reference has no
+ * SEM operator); any fixed order is an equally exact A_e. */
+static double geo3(double ga, double gb, double gc, double ur, double us, double ut) {
+  return fma(gc, ut, fma(gb, us, ga * ur));
+}
+
 static void local_ax(const orc_sem* s, const double* Ge, const double* u, double* out) {
   const int n1 = s->n1, np = s->np;
   const double* D = s->D;
@@ -321,26 +334,26 @@ static void local_ax(const orc_sem* s, const double* Ge, const double* u, double
         const int l = i + n1 * (j + n1 * k);
         double ur = 0, us = 0, ut = 0;
         for (int m = 0; m < n1; ++m) {
-          ur += D[i * n1 + m] * u[m + n1 * (j + n1 * k)];
-          us += D[j * n1 + m] * u[i + n1 * (m + n1 * k)];
-          ut += D[k * n1 + m] * u[i + n1 * (j + n1 * m)];
+          ur = fma(D[i * n1 + m], u[m + n1 * (j + n1 * k)], ur);
+          us = fma(D[j * n1 + m], u[i + n1 * (m + n1 * k)], us);
+          ut = fma(D[k * n1 + m], u[i + n1 * (j + n1 * m)], ut);
         }
         const double grr = Ge[l], grs = Ge[np + l], grt = Ge[2 * np + l];
         const double gss = Ge[3 * np + l], gst = Ge[4 * np + l], gtt = Ge[5 * np + l];
-        wr[l] = grr * ur + grs * us + grt * ut;
-        ws[l] = grs * ur + gss * us + gst * ut;
-        wt[l] = grt * ur + gst * us + gtt * ut;
+        wr[l] = geo3(grr, grs, grt, ur, us, ut);
+        ws[l] = geo3(grs, gss, gst, ur, us, ut);
+        wt[l] = geo3(grt, gst, gtt, ur, us, ut);
       }
   for (int k = 0; k < n1; ++k)
     for (int j = 0; j < n1; ++j)
       for (int i = 0; i < n1; ++i) {
-        double v = 0;
+        double vr = 0, vs = 0, vt = 0;
         for (int m = 0; m < n1; ++m) {
-          v += D[m * n1 + i] * wr[m + n1 * (j + n1 * k)];
-          v += D[m * n1 + j] * ws[i + n1 * (m + n1 * k)];
-          v += D[m * n1 + k] * wt[i + n1 * (j + n1 * m)];
+          vr = fma(D[m * n1 + i], wr[m + n1 * (j + n1 * k)], vr);
+          vs = fma(D[m * n1 + j], ws[i + n1 * (m + n1 * k)], vs);
+          vt = fma(D[m * n1 + k], wt[i + n1 * (j + n1 * m)], vt);
         }
-        out[i + n1 * (j + n1 * k)] = v;
+        out[i + n1 * (j + n1 * k)] = vt + (vr + vs);
       }
 }
 
@@ -356,6 +369,40 @@ static void sem_apply(orc_op* self, const double* x, double* y) {
     for (int l = 0; l < np; ++l)
       if (me[l] >= 0) y[me[l]] += s->wL[l];
   }
+}
+
+/* Element matrices of the assembled operator as (row, col, value) triplets,
+ * one per local pair of non-Dirichlet nodes (duplicates to be summed, as
+ * CsrMatrix::from_triplets does, operators.hpp:80-103).  Returns the count;
+ * NULL outputs only count. */
+size_t orc_sem_local_triplets(const orc_sem* s, int64_t* rows, int64_t* cols, double* vals) {
+  const int np = s->np;
+  size_t cnt = 0;
+  double* u = calloc(np, sizeof(double));
+  double* w = malloc(np * sizeof(double));
+  for (int e = 0; e < s->E; ++e) {
+    const int64_t* me = s->map + (size_t)e * np;
+    for (int b = 0; b < np; ++b) {
+      if (me[b] < 0) continue;
+      if (rows) {
+        memset(u, 0, np * sizeof(double));
+        u[b] = 1.0;
+        local_ax(s, s->G + (size_t)e * 6 * np, u, w);
+      }
+      for (int a = 0; a < np; ++a) {
+        if (me[a] < 0) continue;
+        if (rows) {
+          rows[cnt] = me[a];
+          cols[cnt] = me[b];
+          vals[cnt] = w[a];
+        }
+        ++cnt;
+      }
+    }
+  }
+  free(u);
+  free(w);
+  return cnt;
 }
 
 /* A5 */
@@ -401,7 +448,8 @@ void orc_sem_rhs(const orc_sem* s, double* b) {
   }
 }
 
-/* ---- A6: p-transfers (owner-selection prolongation, exact transpose) ---- */
+/* ---- A6: p-transfers (owner-selection prolongation, exact transpose); the
+ * contractions follow the same fma chain as k_prolong / k_restrict_local ---- */
 static void tensor3(int nf, int nc, const double* J, const double* in, double* out, int transpose) {
   /* out = (J (x) J (x) J) in   (transpose: (J^T (x) J^T (x) J^T) in) ; J is nf x nc */
   double t1[NMAX * NMAX * NMAX], t2[NMAX * NMAX * NMAX];
@@ -412,21 +460,21 @@ static void tensor3(int nf, int nc, const double* J, const double* in, double* o
     for (int j = 0; j < a; ++j)
       for (int i = 0; i < b; ++i) {
         double v = 0;
-        for (int m = 0; m < a; ++m) v += JM(i, m) * in[m + a * (j + a * k)];
+        for (int m = 0; m < a; ++m) v = fma(JM(i, m), in[m + a * (j + a * k)], v);
         t1[i + b * (j + a * k)] = v;
       }
   for (int k = 0; k < a; ++k)
     for (int j = 0; j < b; ++j)
       for (int i = 0; i < b; ++i) {
         double v = 0;
-        for (int m = 0; m < a; ++m) v += JM(j, m) * t1[i + b * (m + a * k)];
+        for (int m = 0; m < a; ++m) v = fma(JM(j, m), t1[i + b * (m + a * k)], v);
         t2[i + b * (j + b * k)] = v;
       }
   for (int k = 0; k < b; ++k)
     for (int j = 0; j < b; ++j)
       for (int i = 0; i < b; ++i) {
         double v = 0;
-        for (int m = 0; m < a; ++m) v += JM(k, m) * t2[i + b * (j + b * m)];
+        for (int m = 0; m < a; ++m) v = fma(JM(k, m), t2[i + b * (j + b * m)], v);
         out[i + b * (j + b * k)] = v;
       }
 #undef JM
@@ -578,6 +626,17 @@ static orc_smoother level_smoother(orc_pmg* p, int l) {
 
 orc_pmg* orc_pmg_create(int nlevels, const int* orders, int Ex, int Ey, int Ez, int geometry,
                         double eps, int smoother, size_t eigen_iterations, uint64_t eigen_seed) {
+  return orc_pmg_create_ex(nlevels, orders, Ex, Ey, Ez, geometry, eps, smoother, eigen_iterations,
+                           eigen_seed, 0);
+}
+
+/* flags: ORC_PMG_NO_LAMBDA skips the lambda estimates (left 0), ORC_PMG_NO_COARSE
+ * the banded Cholesky of the coarsest level -- for oracle/ref_driver.cpp, which
+ * owns both through the reference's own templates (estimate_lambda_max,
+ * BandedCholesky) and only borrows the levels, diagonals and transfers. */
+orc_pmg* orc_pmg_create_ex(int nlevels, const int* orders, int Ex, int Ey, int Ez, int geometry,
+                           double eps, int smoother, size_t eigen_iterations, uint64_t eigen_seed,
+                           int flags) {
   if (nlevels < 1 || nlevels > 8) return NULL;
   orc_pmg* p = calloc(1, sizeof *p);
   p->nlevels = nlevels;
@@ -595,12 +654,12 @@ orc_pmg* orc_pmg_create(int nlevels, const int* orders, int Ex, int Ey, int Ez, 
     p->sch[l].s = p->lev[l];
     p->sch[l].ras = smoother == 2;
   }
-  for (int l = 0; l + 1 < nlevels; ++l) {
+  for (int l = 0; l + 1 < nlevels && !(flags & ORC_PMG_NO_LAMBDA); ++l) {
     orc_smoother S = level_smoother(p, l);
     p->lambda_tilde[l] = orc_estimate_lambda_max(&p->lev[l]->op.base, &S, eigen_iterations, eigen_seed);
     p->lev[l]->op.base.count = 0;
   }
-  if (coarse_factor(p) != 0) {
+  if (!(flags & ORC_PMG_NO_COARSE) && coarse_factor(p) != 0) {
     orc_pmg_destroy(p);
     return NULL;
   }

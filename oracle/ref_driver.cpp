@@ -10,6 +10,7 @@
 // the reference's LinearOperatorLike concept (operators.hpp:19-26) so that the
 // reference's smoother and Krylov templates drive it -- the CPU baseline the
 // survey prescribes.
+#include <chebmg/cholesky.hpp>
 #include <chebmg/harness.hpp>
 #include <chebmg/io.hpp>
 #include <chebmg/krylov.hpp>
@@ -19,10 +20,13 @@
 #include <chebmg/smoothers.hpp>
 
 #include <algorithm>
+#include <memory>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <tuple>
+#include <vector>
 
 extern "C" {
 #include "oracle.h"
@@ -358,6 +362,207 @@ int ref_sem_solve(void* pmg, int driver, int family, double lmax_mult, double lm
     fill_report(res.second, hist, hist_cap, hist_len, its, mv, converged, status, rho, wall);
   });
 }
+
+// ---- SEM p-multigrid on the reference's own templates ----
+//
+// The reference's CPU path for the north-star solve, as literally as the
+// reference allows: its pgmres/pcg (krylov.hpp:75-264) drive A; the
+// preconditioner is its v_cycle (multigrid.hpp:69-90) generalised to several
+// p-levels -- chebyshev_smooth (smoothers.hpp:156-172), residual_into
+// (:83-91), axpy, the x = corr assign rule -- with jacobi_inverse_diagonal
+// (:174-181), estimate_lambda_max (:61-79) and, on the coarsest level, the
+// reference's BandedCholesky (cholesky.hpp:18-91) of the assembled operator
+// (CsrMatrix::from_triplets, operators.hpp:80-103).  Only the pieces the
+// reference has no code for come from the restatement: the SEM operator and
+// its diagonal, the p-transfers, and (for ASM/RAS) the Schwarz smoother with
+// its generic-S Chebyshev recurrence.
+struct RefPmg {
+  orc_pmg* p = nullptr;
+  int nl = 0, smoother = 0;
+  std::vector<SemOperator> A;
+  std::vector<Vec> inv_diag;
+  std::vector<double> lambda;
+  std::vector<orc_schwarz_ctx> sch;
+  std::unique_ptr<BandedCholesky> coarse;
+
+  void vcycle(int l, const ChebyshevConfig& base, std::size_t kpre, std::size_t kpost, const Vec& b, Vec& x,
+              bool x_is_zero) const {
+    const SemOperator& Al = A[l];
+    const std::size_t n = Al.rows();
+    if (l == nl - 1) {  // exact coarse solve (multigrid.hpp:78)
+      if (x_is_zero) {
+        coarse->solve(b, x);
+      } else {
+        Vec r(n), e(n);
+        detail::residual_into(Al, b, x, false, r);
+        coarse->solve(r, e);
+        axpy(1.0, e, x);
+      }
+      return;
+    }
+    ChebyshevConfig cfg = base;
+    cfg.lambda_tilde = lambda[l];
+    auto smooth = [&](std::size_t k, Vec& xv, bool xz) {
+      if (smoother == 0) {
+        chebyshev_smooth(Al, inv_diag[l], cfg, k, b, xv, xz);
+      } else {  // Schwarz S: the restated generic-S recurrence (no reference code)
+        orc_smoother S{nullptr, orc_sem_schwarz_apply_cb, const_cast<orc_schwarz_ctx*>(&sch[l])};
+        orc_cheb_config c{static_cast<int>(cfg.family), cfg.lambda_tilde, cfg.lambda_max_multiplier,
+                          cfg.lambda_min_multiplier};
+        orc_op* op = orc_pmg_op(p, l);
+        if (orc_chebyshev_smooth(op, &S, &c, k, b.data(), xv.data(), xz ? 1 : 0))
+          throw std::invalid_argument("schwarz smoother: invalid configuration");
+      }
+    };
+    if (kpre > 0) {
+      smooth(kpre, x, x_is_zero);
+      x_is_zero = false;
+    }
+    Vec r(n);
+    detail::residual_into(Al, b, x, x_is_zero, r);
+    const std::size_t nc = A[l + 1].rows();
+    Vec rc(nc), ec(nc, 0.0), corr(n);
+    orc_sem_restrict(orc_pmg_sem(p, l), orc_pmg_sem(p, l + 1), r.data(), rc.data());
+    vcycle(l + 1, base, kpre, kpost, rc, ec, true);
+    orc_sem_prolong(orc_pmg_sem(p, l), orc_pmg_sem(p, l + 1), ec.data(), corr.data());
+    if (x_is_zero) {
+      x = corr;
+    } else {
+      axpy(1.0, corr, x);
+    }
+    if (kpost > 0) smooth(kpost, x, false);
+  }
+};
+
+extern "C" {
+
+// levels/diagonals/transfers from the restatement, everything else reference
+void* ref_pmg_create(int nlevels, const int* orders, int Ex, int Ey, int Ez, int geometry, double eps,
+                     int smoother, std::size_t eig_iters, std::uint64_t seed) {
+  try {
+    auto* R = new RefPmg;
+    R->p = orc_pmg_create_ex(nlevels, orders, Ex, Ey, Ez, geometry, eps, smoother, eig_iters, seed,
+                             ORC_PMG_NO_LAMBDA | ORC_PMG_NO_COARSE);
+    if (!R->p) throw std::invalid_argument("orc_pmg_create_ex failed");
+    R->nl = nlevels;
+    R->smoother = smoother;
+    R->sch.resize(nlevels);
+    for (int l = 0; l < nlevels; ++l) {
+      R->A.emplace_back(orc_pmg_op(R->p, l), orc_pmg_sem(R->p, l));
+      R->inv_diag.push_back(jacobi_inverse_diagonal(R->A[l].diagonal()));
+      R->sch[l] = orc_schwarz_ctx{orc_pmg_sem(R->p, l), smoother == 2};
+    }
+    R->lambda.assign(nlevels, 0.0);
+    for (int l = 0; l + 1 < nlevels; ++l) {
+      if (smoother == 0) {
+        R->lambda[l] = estimate_lambda_max(R->A[l], R->inv_diag[l], eig_iters, seed);
+      } else {
+        orc_smoother S{nullptr, orc_sem_schwarz_apply_cb, &R->sch[l]};
+        R->lambda[l] = orc_estimate_lambda_max(orc_pmg_op(R->p, l), &S, eig_iters, seed);
+      }
+      R->A[l].reset_applications();
+    }
+    orc_sem* c = orc_pmg_sem(R->p, nlevels - 1);
+    const std::size_t cnt = orc_sem_local_triplets(c, nullptr, nullptr, nullptr);
+    std::vector<std::int64_t> rr(cnt), cc(cnt);
+    std::vector<double> vv(cnt);
+    orc_sem_local_triplets(c, rr.data(), cc.data(), vv.data());
+    std::vector<std::tuple<std::size_t, std::size_t, double>> trip(cnt);
+    for (std::size_t t = 0; t < cnt; ++t) trip[t] = {std::size_t(rr[t]), std::size_t(cc[t]), vv[t]};
+    const std::size_t nc = orc_sem_n(c);
+    R->coarse = std::make_unique<BandedCholesky>(CsrMatrix::from_triplets(nc, nc, std::move(trip)));
+    return R;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_pmg_destroy(void* h) {
+  auto* R = static_cast<RefPmg*>(h);
+  if (R) orc_pmg_destroy(R->p);
+  delete R;
+}
+
+void* ref_pmg_levels(void* h) { return static_cast<RefPmg*>(h)->p; }
+double ref_pmg_lambda(void* h, int l) { return static_cast<RefPmg*>(h)->lambda[l]; }
+std::size_t ref_pmg_coarse_bandwidth(void* h) { return static_cast<RefPmg*>(h)->coarse->bandwidth(); }
+
+int ref_pmg_coarse_solve(void* h, const double* b, double* x) {
+  auto* R = static_cast<RefPmg*>(h);
+  return guarded([&] {
+    const std::size_t n = R->coarse->size();
+    Vec bv(b, b + n), xv(n);
+    R->coarse->solve(bv, xv);
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+// preconditioner_apply (multigrid.hpp:94-98): one V-cycle from x = 0
+int ref_pmg_v_cycle(void* h, int family, double lmax_mult, double lmin_mult, std::size_t k_pre,
+                    std::size_t k_post, const double* b, double* x) {
+  auto* R = static_cast<RefPmg*>(h);
+  return guarded([&] {
+    ChebyshevConfig s;
+    s.family = fam(family);
+    s.lambda_max_multiplier = lmax_mult;
+    s.lambda_min_multiplier = lmin_mult;
+    const std::size_t n = R->A[0].rows();
+    Vec bv(b, b + n), xv(n, 0.0);
+    R->vcycle(0, s, k_pre, k_post, bv, xv, true);
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+// Chebyshev sweep on one level (Jacobi: chebyshev_smooth template)
+int ref_pmg_smooth(void* h, int level, int family, std::size_t order, double lmax_mult, double lmin_mult,
+                   const double* b, double* x, int x_is_zero, std::size_t* apps) {
+  auto* R = static_cast<RefPmg*>(h);
+  return guarded([&] {
+    ChebyshevConfig cfg;
+    cfg.family = fam(family);
+    cfg.lambda_tilde = R->lambda[level];
+    cfg.lambda_max_multiplier = lmax_mult;
+    cfg.lambda_min_multiplier = lmin_mult;
+    const std::size_t n = R->A[level].rows();
+    Vec bv(b, b + n), xv(x, x + n);
+    const std::size_t a0 = R->A[level].applications();
+    chebyshev_smooth(R->A[level], R->inv_diag[level], cfg, order, bv, xv, x_is_zero != 0);
+    *apps = R->A[level].applications() - a0;
+    std::memcpy(x, xv.data(), n * sizeof(double));
+  });
+}
+
+// pgmres (driver 1) / pcg (driver 0) with the reference-template p-MG V-cycle, x0 = 0
+int ref_pmg_solve(void* h, int driver, int family, double lmax_mult, double lmin_mult, std::size_t k_pre,
+                  std::size_t k_post, const double* b, double tol, std::size_t maxit, std::size_t restart,
+                  double* x_out, double* hist, std::size_t hist_cap, std::size_t* hist_len, std::size_t* its,
+                  std::size_t* mv, int* converged, char* status, double* rho, double* wall) {
+  auto* R = static_cast<RefPmg*>(h);
+  return guarded([&] {
+    ChebyshevConfig s;
+    s.family = fam(family);
+    s.lambda_max_multiplier = lmax_mult;
+    s.lambda_min_multiplier = lmin_mult;
+    const SemOperator& A = R->A[0];
+    const std::size_t n = A.rows();
+    const Preconditioner M = [&](const Vec& v) {
+      Vec z(n, 0.0);
+      R->vcycle(0, s, k_pre, k_post, v, z, true);
+      return z;
+    };
+    const Vec bv(b, b + n), x0(n, 0.0);
+    SolveOptions o;
+    o.tol = tol;
+    o.maxit = maxit;
+    o.restart = restart;
+    std::pair<Vec, SolveReport> res = driver == 0 ? pcg(A, M, bv, x0, o) : pgmres(A, M, bv, x0, o);
+    std::memcpy(x_out, res.first.data(), n * sizeof(double));
+    fill_report(res.second, hist, hist_cap, hist_len, its, mv, converged, status, rho, wall);
+  });
+}
+
+}  // extern "C"
 
 // ---- io.hpp text formats (checker for paper_2210_03179_b200/io.py) ----
 

@@ -118,6 +118,10 @@ _protos = {
     "cmg_sem_gs_map_host": (C.c_int, [C.POINTER(SemDesc), C.POINTER(C.c_int64)]),
     "cmg_sem_local_slots": (sz, [C.POINTER(SemDesc)]),
     "cmg_sem_rhs": (C.c_int, [vp, vp]),
+    "cmg_sem_basis_host": (C.c_int, [C.c_int, vp, vp, vp]),
+    "cmg_sem_interp_host": (C.c_int, [C.c_int, C.c_int, vp]),
+    "cmg_sem_fdm1d_host": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, vp, vp]),
     "cmg_pmg_create": (C.c_int, [vp, C.POINTER(SemDesc), C.c_int, C.POINTER(C.c_int), C.c_int, sz, u64,
                                  C.POINTER(vp)]),
     "cmg_pmg_destroy": (C.c_int, [vp]),

@@ -1,7 +1,11 @@
 // k_schwarz.cu -- Chebyshev-Schwarz smoother kernels (PAPER.md:560-629,
 // SURVEY App. A8): overlapping (N+3)^3 extended-element subdomains solved
 // exactly by fast diagonalisation, combined additively (ASM, post-weighted)
-// or restrictively (RAS).  The definition matches oracle/oracle_schwarz.c.
+// or restrictively (RAS).  The definition matches oracle/oracle_schwarz.c,
+// and so does the rounding: this file is built with --fmad=false and every
+// mode-product output is one __fma_rn chain over ascending m, as the oracle's
+// fma() chain, so the CUDA-core local solves are bit-identical to it (the
+// opt-in DMMA variant, CMG_SCHWARZ_MMA=1, is not).
 #include <cstdlib>
 
 #include "sem_kernels.hpp"
@@ -95,10 +99,10 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
 #pragma unroll
           for (int m = 0; m < PB; ++m) {
             const double2 sp = *reinterpret_cast<const double2*>(Sd + m * PB + o);
-            a0 += sp.x * v1[m];
-            a1 += sp.y * v1[m];
-            c0 += sp.x * v2[m];
-            c1 += sp.y * v2[m];
+            a0 = __fma_rn(sp.x, v1[m], a0);
+            a1 = __fma_rn(sp.y, v1[m], a1);
+            c0 = __fma_rn(sp.x, v2[m], c0);
+            c1 = __fma_rn(sp.y, v2[m], c1);
           }
           if (dim == 2) {
             a0 /= (lam[0][l % PB] + lam[1][l / PB] + lam[2][o]);
@@ -120,8 +124,8 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
 #pragma unroll
           for (int m = 0; m < PB; ++m) {
             const double sv = Sd[m * PB + o];
-            a0 += sv * v1[m];
-            c0 += sv * v2[m];
+            a0 = __fma_rn(sv, v1[m], a0);
+            c0 = __fma_rn(sv, v2[m], c0);
           }
           if (dim == 2) {
             a0 /= (lam[0][l % PB] + lam[1][l / PB] + lam[2][o]);
@@ -158,17 +162,17 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
 #pragma unroll
           for (int m = 0; m < PB; m += 2) {
             const double2 sp = *reinterpret_cast<const double2*>(Sd + o * PB + m);
-            a0 += sp.x * v1[m];
-            a0 += sp.y * v1[m + 1];
-            c0 += sp.x * v2[m];
-            c0 += sp.y * v2[m + 1];
+            a0 = __fma_rn(sp.x, v1[m], a0);
+            a0 = __fma_rn(sp.y, v1[m + 1], a0);
+            c0 = __fma_rn(sp.x, v2[m], c0);
+            c0 = __fma_rn(sp.y, v2[m + 1], c0);
           }
         } else {
 #pragma unroll
           for (int m = 0; m < PB; ++m) {
             const double sv = Sd[o * PB + m];
-            a0 += sv * v1[m];
-            c0 += sv * v2[m];
+            a0 = __fma_rn(sv, v1[m], a0);
+            c0 = __fma_rn(sv, v2[m], c0);
           }
         }
         out[b1 + o * st] = a0;
@@ -243,8 +247,8 @@ __global__ void __launch_bounds__(EPB * (N + 3) * (N + 3)) k_schwarz_local_small
 #pragma unroll
             for (int m = 0; m < PB; ++m) {
               const double2 sp = *reinterpret_cast<const double2*>(Sd + m * PB + o);
-              a0 += sp.x * v[m];
-              a1 += sp.y * v[m];
+              a0 = __fma_rn(sp.x, v[m], a0);
+              a1 = __fma_rn(sp.y, v[m], a1);
             }
             if (pass == 2) {
               a0 /= (lam[le][0][p] + lam[le][1][q] + lam[le][2][o]);
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(EPB * (N + 3) * (N + 3)) k_schwarz_local_small
           for (int o = 0; o < PB; ++o) {
             double a0 = 0.0;
 #pragma unroll
-            for (int m = 0; m < PB; ++m) a0 += Sd[m * PB + o] * v[m];
+            for (int m = 0; m < PB; ++m) a0 = __fma_rn(Sd[m * PB + o], v[m], a0);
             if (pass == 2) a0 /= (lam[le][0][p] + lam[le][1][q] + lam[le][2][o]);
             out[b1 + o * st] = a0;
           }
@@ -271,12 +275,12 @@ __global__ void __launch_bounds__(EPB * (N + 3) * (N + 3)) k_schwarz_local_small
 #pragma unroll
             for (int m = 0; m < PB; m += 2) {
               const double2 sp = *reinterpret_cast<const double2*>(Sd + o * PB + m);
-              a0 += sp.x * v[m];
-              a0 += sp.y * v[m + 1];
+              a0 = __fma_rn(sp.x, v[m], a0);
+              a0 = __fma_rn(sp.y, v[m + 1], a0);
             }
           } else {
 #pragma unroll
-            for (int m = 0; m < PB; ++m) a0 += Sd[o * PB + m] * v[m];
+            for (int m = 0; m < PB; ++m) a0 = __fma_rn(Sd[o * PB + m], v[m], a0);
           }
           out[b1 + o * st] = a0;
         }

@@ -78,6 +78,20 @@ __device__ __forceinline__ int owner1d(int ec, int l, int ne, int& oe) {
   return (g - 1) - oe * N;
 }
 
+// ---------------------------------------------------------------- arithmetic contract
+// This file is compiled with --fmad=false (Makefile): the only fused
+// multiply-adds are the explicit __fma_rn calls, placed exactly where
+// oracle/oracle_sem.c calls C99 fma(), so the local operator, its diagonal,
+// the p-transfers and the Chebyshev epilogues round identically on the GPU
+// and in the CPU restatement (bitwise):
+//   1D contraction  v = 0; for m ascending: v = fma(D_m, u_m, v)
+//   geometry        w_a = fma(g_c, u_t, fma(g_b, u_s, g_a * u_r))
+//   divergence      out = v_t + (v_r + v_s)       (three separate chains)
+//   everything else: the reference's operand order without contraction.
+__device__ __forceinline__ double geo3(double ga, double gb, double gc, double ur, double us, double ut) {
+  return __fma_rn(gc, ut, __fma_rn(gb, us, ga * ur));
+}
+
 // ---------------------------------------------------------------- epilogues
 template <int EPI>
 struct EpiOps {  // slot-vector operands read for interior nodes, in smem order
@@ -239,15 +253,15 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
     double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
-      ur += sD[i][m] * ue[(k * N1 + j) * N1 + m];
-      us += sD[j][m] * ue[(k * N1 + m) * N1 + i];
-      ut += sD[k][m] * ue[(m * N1 + j) * N1 + i];
+      ur = __fma_rn(sD[i][m], ue[(k * N1 + j) * N1 + m], ur);
+      us = __fma_rn(sD[j][m], ue[(k * N1 + m) * N1 + i], us);
+      ut = __fma_rn(sD[k][m], ue[(m * N1 + j) * N1 + i], ut);
     }
     const double g0 = Ge[l], g1 = Ge[NP + l], g2 = Ge[2 * NP + l];
     const double g3 = Ge[3 * NP + l], g4 = Ge[4 * NP + l], g5 = Ge[5 * NP + l];
-    Ge[l] = g0 * ur + g1 * us + g2 * ut;
-    Ge[NP + l] = g1 * ur + g3 * us + g4 * ut;
-    Ge[2 * NP + l] = g2 * ur + g4 * us + g5 * ut;
+    Ge[l] = geo3(g0, g1, g2, ur, us, ut);
+    Ge[NP + l] = geo3(g1, g3, g4, ur, us, ut);
+    Ge[2 * NP + l] = geo3(g2, g4, g5, ur, us, ut);
   }
   __syncthreads();
   if (!active) return;
@@ -257,13 +271,14 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
 #pragma unroll
   for (int kk = 0; kk < KN; ++kk) {
     const int k = kb + kk;
-    double v = 0.0;
+    double vr = 0.0, vs = 0.0, vt = 0.0;
 #pragma unroll
     for (int m = 0; m < N1; ++m) {
-      v += sD[m][i] * Ge[(k * N1 + j) * N1 + m];
-      v += sD[m][j] * Ge[NP + (k * N1 + m) * N1 + i];
-      v += sD[m][k] * Ge[2 * NP + (m * N1 + j) * N1 + i];
+      vr = __fma_rn(sD[m][i], Ge[(k * N1 + j) * N1 + m], vr);
+      vs = __fma_rn(sD[m][j], Ge[NP + (k * N1 + m) * N1 + i], vs);
+      vt = __fma_rn(sD[m][k], Ge[2 * NP + (m * N1 + j) * N1 + i], vt);
     }
+    const double v = vt + (vr + vs);
     if (ij_interior && k >= 1 && k < N) {
       const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
       const double dv = ue[(k * N1 + j) * N1 + i];
@@ -783,7 +798,7 @@ __global__ void __launch_bounds__(128) k_prolong(SemArgs F, SemArgs Cc, const do
     const int le = qq / T1, q = qq - le * T1;
     const int i = q % F1, b = (q / F1) % C1, c = q / (F1 * C1);
     double v = 0.0;
-    for (int m = 0; m < C1; ++m) v += sJ[i * C1 + m] * uc[le][m + C1 * (b + C1 * c)];
+    for (int m = 0; m < C1; ++m) v = __fma_rn(sJ[i * C1 + m], uc[le][m + C1 * (b + C1 * c)], v);
     t1[le][q] = v;
   }
   __syncthreads();
@@ -791,7 +806,7 @@ __global__ void __launch_bounds__(128) k_prolong(SemArgs F, SemArgs Cc, const do
     const int le = qq / T2, q = qq - le * T2;
     const int i = q % F1, j = (q / F1) % F1, c = q / (F1 * F1);
     double v = 0.0;
-    for (int m = 0; m < C1; ++m) v += sJ[j * C1 + m] * t1[le][i + F1 * (m + C1 * c)];
+    for (int m = 0; m < C1; ++m) v = __fma_rn(sJ[j * C1 + m], t1[le][i + F1 * (m + C1 * c)], v);
     t2[le][q] = v;
   }
   __syncthreads();
@@ -804,7 +819,7 @@ __global__ void __launch_bounds__(128) k_prolong(SemArgs F, SemArgs Cc, const do
     const int i = a + 1, j = b + 1, k = c + 1;
     if (ex * NF + i >= NF * F.Ex || ey * NF + j >= NF * F.Ey || (F.z0 + ez) * NF + k >= NF * F.Ez) continue;
     double v = 0.0;
-    for (int m = 0; m < C1; ++m) v += sJ[k * C1 + m] * t2[le][i + F1 * (j + F1 * m)];
+    for (int m = 0; m < C1; ++m) v = __fma_rn(sJ[k * C1 + m], t2[le][i + F1 * (j + F1 * m)], v);
     const long slot = e * NOSF + sem_pos(NF, a, b, c);
     yf[slot] = add ? yf[slot] + v : v;
   }
@@ -835,7 +850,7 @@ __global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double*
     const int le = qq / T1, q = qq - le * T1;
     const int a = q % C1, j = (q / C1) % F1, k = q / (C1 * F1);
     double v = 0.0;
-    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + a] * uf[le][m + F1 * (j + F1 * k)];
+    for (int m = 0; m < F1; ++m) v = __fma_rn(sJ[m * C1 + a], uf[le][m + F1 * (j + F1 * k)], v);
     t1[le][q] = v;
   }
   __syncthreads();
@@ -843,7 +858,7 @@ __global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double*
     const int le = qq / T2, q = qq - le * T2;
     const int a = q % C1, b = (q / C1) % C1, k = q / (C1 * C1);
     double v = 0.0;
-    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + b] * t1[le][a + C1 * (m + F1 * k)];
+    for (int m = 0; m < F1; ++m) v = __fma_rn(sJ[m * C1 + b], t1[le][a + C1 * (m + F1 * k)], v);
     t2[le][q] = v;
   }
   __syncthreads();
@@ -853,7 +868,7 @@ __global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double*
     if (e >= E) continue;
     const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
     double v = 0.0;
-    for (int m = 0; m < F1; ++m) v += sJ[m * C1 + c] * t2[le][a + C1 * (b + C1 * m)];
+    for (int m = 0; m < F1; ++m) v = __fma_rn(sJ[m * C1 + c], t2[le][a + C1 * (b + C1 * m)], v);
     Lc[e * CP + q] = v;
   }
 }

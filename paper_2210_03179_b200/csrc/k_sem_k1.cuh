@@ -64,7 +64,7 @@ struct K1L {
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += c_D[N][(O0 + q) * N1 + m] * l[m];
+      for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][(O0 + q) * N1 + m], l[m], v);
       sr[idx(O0 + q, ta, tb)] = v;
     }
 #pragma unroll
@@ -73,7 +73,7 @@ struct K1L {
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += c_D[N][(O0 + q) * N1 + m] * l[m];
+      for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][(O0 + q) * N1 + m], l[m], v);
       ss[idx(ta, O0 + q, tb)] = v;
     }
 #pragma unroll
@@ -82,7 +82,7 @@ struct K1L {
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += c_D[N][(O0 + q) * N1 + m] * l[m];
+      for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][(O0 + q) * N1 + m], l[m], v);
       wt[q] = v;
       dvh[q] = l[O0 + q];
     }
@@ -98,9 +98,9 @@ struct K1L {
       const double ur = sr[idx(i, j, k)], us = ss[idx(i, j, k)], ut = wt[q];
       const double g0 = sG[l], g1 = sG[NP + l], g2 = sG[2 * NP + l];
       const double g3 = sG[3 * NP + l], g4 = sG[4 * NP + l], g5 = sG[5 * NP + l];
-      sr[idx(i, j, k)] = g0 * ur + g1 * us + g2 * ut;
-      ss[idx(i, j, k)] = g1 * ur + g3 * us + g4 * ut;
-      wt[q] = g2 * ur + g4 * us + g5 * ut;
+      sr[idx(i, j, k)] = geo3(g0, g1, g2, ur, us, ut);
+      ss[idx(i, j, k)] = geo3(g1, g3, g4, ur, us, ut);
+      wt[q] = geo3(g2, g4, g5, ur, us, ut);
     }
   }
 
@@ -121,9 +121,9 @@ struct K1L {
     for (int q = 0; q < KH; ++q) {
       const int k = O0 + q;
       const double ur = sr[idx(i, j, k)], us = ss[idx(i, j, k)], ut = wt[q];
-      sr[idx(i, j, k)] = g[0][q] * ur + g[1][q] * us + g[2][q] * ut;
-      ss[idx(i, j, k)] = g[1][q] * ur + g[3][q] * us + g[4][q] * ut;
-      wt[q] = g[2][q] * ur + g[4][q] * us + g[5][q] * ut;
+      sr[idx(i, j, k)] = geo3(g[0][q], g[1][q], g[2][q], ur, us, ut);
+      ss[idx(i, j, k)] = geo3(g[1][q], g[3][q], g[4][q], ur, us, ut);
+      wt[q] = geo3(g[2][q], g[4][q], g[5][q], ur, us, ut);
     }
   }
 
@@ -137,7 +137,7 @@ struct K1L {
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += c_D[N][m * N1 + (O0 + q)] * l[m];
+      for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][m * N1 + (O0 + q)], l[m], v);
       su[idx(O0 + q, ta, tb)] = v;
     }
   }
@@ -154,7 +154,7 @@ struct K1L {
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += c_D[N][m * N1 + (O0 + q)] * l[m];
+      for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][m * N1 + (O0 + q)], l[m], v);
       su[idx(ta, O0 + q, tb)] += v;
     }
   }
@@ -172,7 +172,7 @@ struct K1L {
       const int k = O0 + q;
       double v = 0.0;
 #pragma unroll
-      for (int m = 0; m < N1; ++m) v += c_D[N][m * N1 + k] * l[m];
+      for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][m * N1 + k], l[m], v);
       v += su[idx(i, j, k)];
       if (ij_interior && k >= 1 && k < N) {
         const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));

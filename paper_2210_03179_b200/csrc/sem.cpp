@@ -1332,6 +1332,32 @@ size_t cmg_sem_local_slots(const cmg_sem_desc* d) {
   return static_cast<size_t>(d->ex) * d->ey * (z1 - z0) * sem_nos(d->order);
 }
 
+int cmg_sem_basis_host(int N, double* xi, double* w, double* D) {
+  return guard([&] {
+    if (N < 1 || N > 7) fail(CMG_EINVAL, "sem_basis_host: order must be 1..7");
+    host_gll(N, xi, w);
+    host_deriv_matrix(N, xi, D);
+  });
+}
+
+int cmg_sem_interp_host(int Nf, int Nc, double* J) {
+  return guard([&] {
+    if (Nf < 1 || Nf > 7 || Nc < 1 || Nc > Nf) fail(CMG_EINVAL, "sem_interp_host: need 1 <= Nc <= Nf <= 7");
+    host_interp_matrix(Nf, Nc, J);
+  });
+}
+
+int cmg_sem_fdm1d_host(int N, double Ll, double L, double Lr, int dl, int d0, int dN, int dr, double* S,
+                       double* lam) {
+  return guard([&] {
+    if (N < 2 || N > 7) fail(CMG_EINVAL, "sem_fdm1d_host: order must be 2..7");
+    std::vector<double> xi(N + 1), w(N + 1), D((N + 1) * (N + 1));
+    host_gll(N, xi.data(), w.data());
+    host_deriv_matrix(N, xi.data(), D.data());
+    host_fdm_1d(N, w.data(), D.data(), Ll, L, Lr, dl, d0, dN, dr, S, lam);
+  });
+}
+
 int cmg_sem_slot_map_host(const cmg_sem_desc* d, int64_t* map) {
   return guard([&] {
     validate_desc(*d);

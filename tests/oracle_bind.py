@@ -490,3 +490,87 @@ def ref_sem_solve(pmg: OraclePmg, driver, family, kpre, kpost, b, tol=1e-8, maxi
     assert rc == 0, R.ref_last_error()
     return Report(its.value, mv.value, hist[: hl.value].tolist(), bool(cv.value), st.value.decode(), rho.value,
                   wall_time_sec=wall.value, x=x)
+
+
+class RefPmg:
+    """p-MG on the reference's own templates (oracle/ref_driver.cpp RefPmg):
+    pgmres/pcg, chebyshev_smooth, residual_into, estimate_lambda_max and the
+    BandedCholesky coarse solve; SEM levels, diagonals and transfers from the
+    restatement."""
+
+    def __init__(self, orders, ex, ey, ez, geometry=0, eps=1.0, smoother=0, eig_iters=30, seed=7):
+        R = ref()
+        _sem_protos(R)
+        R.ref_pmg_create.restype = C.c_void_p
+        R.ref_pmg_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                     C.c_int, sz, C.c_uint64]
+        R.ref_pmg_destroy.argtypes = [C.c_void_p]
+        R.ref_pmg_levels.restype = C.c_void_p
+        R.ref_pmg_levels.argtypes = [C.c_void_p]
+        R.ref_pmg_lambda.restype = C.c_double
+        R.ref_pmg_lambda.argtypes = [C.c_void_p, C.c_int]
+        R.ref_pmg_coarse_bandwidth.restype = sz
+        R.ref_pmg_coarse_bandwidth.argtypes = [C.c_void_p]
+        R.ref_pmg_coarse_solve.argtypes = [C.c_void_p, dp, dp]
+        R.ref_pmg_v_cycle.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, sz, sz, dp, dp]
+        R.ref_pmg_smooth.argtypes = [C.c_void_p, C.c_int, C.c_int, sz, C.c_double, C.c_double, dp, dp, C.c_int,
+                                     C.POINTER(sz)]
+        R.ref_pmg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, sz, sz, dp, C.c_double,
+                                    sz, sz, dp, dp, sz, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz),
+                                    C.POINTER(C.c_int), C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        self.R = R
+        self.L = R
+        self.orders = list(orders)
+        arr = (C.c_int * len(orders))(*orders)
+        self.h = R.ref_pmg_create(len(orders), arr, ex, ey, ez, geometry, eps, smoother, eig_iters, seed)
+        if not self.h:
+            raise ValueError(R.ref_last_error().decode())
+        self.p = R.ref_pmg_levels(self.h)
+        self.lambda_tilde = [R.ref_pmg_lambda(self.h, l) for l in range(len(orders))]
+        self.n = [R.orc_sem_n(R.orc_pmg_sem(self.p, l)) for l in range(len(orders))]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.R.ref_pmg_destroy(self.h)
+
+    def sem(self, level):
+        return OraclePmg.sem(self, level)
+
+    def prolong(self, level, xc):
+        return OraclePmg.prolong(self, level, xc)
+
+    def restrict(self, level, xf):
+        return OraclePmg.restrict(self, level, xf)
+
+    def coarse_solve(self, rc):
+        e = np.empty_like(rc)
+        assert self.R.ref_pmg_coarse_solve(self.h, P(np.ascontiguousarray(rc)), P(e)) == 0
+        return e
+
+    def v_cycle(self, family, kpre, kpost, b, lmaxm=1.03, lminm=0.1):
+        x = np.zeros(self.n[0])
+        rc = self.R.ref_pmg_v_cycle(self.h, family, lmaxm, lminm, kpre, kpost, P(np.ascontiguousarray(b)), P(x))
+        assert rc == 0, self.R.ref_last_error()
+        return x
+
+    def smooth(self, level, family, order, b, x, x_is_zero, lmaxm=1.03, lminm=0.1):
+        x = np.array(x, dtype=np.float64)
+        apps = sz()
+        rc = self.R.ref_pmg_smooth(self.h, level, family, order, lmaxm, lminm, P(np.ascontiguousarray(b)), P(x),
+                                   1 if x_is_zero else 0, C.byref(apps))
+        assert rc == 0, self.R.ref_last_error()
+        return x, apps.value
+
+    def solve(self, driver, family, kpre, kpost, b, tol=1e-8, maxit=500, restart=30, lmaxm=1.03, lminm=0.1):
+        x = np.zeros(self.n[0])
+        hist = np.zeros(maxit + 2)
+        hl, its, mv = sz(), sz(), sz()
+        cv = C.c_int()
+        st = C.create_string_buffer(128)
+        rho, wall = C.c_double(), C.c_double()
+        rc = self.R.ref_pmg_solve(self.h, driver, family, lmaxm, lminm, kpre, kpost, P(np.ascontiguousarray(b)),
+                                  tol, maxit, restart, P(x), P(hist), maxit + 2, C.byref(hl), C.byref(its),
+                                  C.byref(mv), C.byref(cv), st, C.byref(rho), C.byref(wall))
+        assert rc == 0, self.R.ref_last_error()
+        return Report(its.value, mv.value, hist[: hl.value].tolist(), bool(cv.value), st.value.decode(), rho.value,
+                      wall_time_sec=wall.value, x=x)

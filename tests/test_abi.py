@@ -69,3 +69,40 @@ def test_domain_validation():
             raise AssertionError("expected ValueError")
         except ValueError:
             pass
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def test_sem_host_tables_bitwise_equal_oracle():
+    """The GLL basis, derivative and interpolation matrices and the 1D Schwarz
+    FDM bases the device operators are built from are bit-identical to the
+    restatement's (oracle_sem.c / oracle_schwarz.c) -- the precondition for the
+    bitwise operator/transfer/local-solve comparisons in the -m gpu tests."""
+    from paper_2210_03179_b200 import _lib
+
+    L = ob.oracle()
+    ob._sem_protos(L)
+    L.orc_fdm_1d.argtypes = [C.c_int, ob.dp, ob.dp, ob.dp, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                             C.c_int, C.c_int, ob.dp, ob.dp]
+    for N in range(1, 8):
+        xi, w, D = np.empty(N + 1), np.empty(N + 1), np.empty((N + 1) ** 2)
+        assert _lib.lib.cmg_sem_basis_host(N, _dp(xi), _dp(w), _dp(D)) == 0
+        oxi, ow, oD = ob.gll(N)
+        assert xi.tobytes() == oxi.tobytes() and w.tobytes() == ow.tobytes()
+        assert D.tobytes() == oD.reshape(-1).tobytes()
+        for Nc in range(1, N + 1):
+            J = np.empty((N + 1) * (Nc + 1))
+            assert _lib.lib.cmg_sem_interp_host(N, Nc, _dp(J)) == 0
+            assert J.tobytes() == ob.interp_matrix(N, Nc).reshape(-1).tobytes()
+    for N in (2, 3, 5, 7):
+        xi, w, D = ob.gll(N)
+        D = np.ascontiguousarray(D.reshape(-1))
+        for lens in ((0.1, 0.1, 0.1), (0.07, 0.13, 0.21)):
+            for flags in ((0, 0, 0, 0), (1, 1, 0, 0), (1, 0, 0, 0), (0, 0, 1, 1), (0, 0, 0, 1)):
+                S, lam = np.empty((N + 3) ** 2), np.empty(N + 3)
+                oS, olam = np.empty((N + 3) ** 2), np.empty(N + 3)
+                assert _lib.lib.cmg_sem_fdm1d_host(N, *lens, *flags, _dp(S), _dp(lam)) == 0
+                L.orc_fdm_1d(N, ob.P(xi), ob.P(w), ob.P(D), *lens, *flags, ob.P(oS), ob.P(olam))
+                assert S.tobytes() == oS.tobytes() and lam.tobytes() == olam.tobytes(), (N, lens, flags)

@@ -1,12 +1,22 @@
-"""SEM p-multigrid path on the GPU vs the oracle restatement (and the reference's
-own Krylov templates driving it, oracle/_ref).  Tolerances in fp64: operator /
-transfer / smoother outputs 1e-12..1e-11 relative (different but fixed
-summation order), iteration counts and fine_matvecs exact, residual histories
-within 1e-10 relative to the initial residual (the normalised history
-||r_k||/||r_0|| the solver tests against tol) and solutions within 1e-10
-relative (BASELINE north_star).  Per-entry relative agreement of the tail of a
-1e-8-converged history is not attainable by any re-ordered fp64 arithmetic
-(every perturbation is amplified by ||r_0||/||r_k||); see DESIGN.md §5."""
+"""SEM p-multigrid path on the GPU vs the restatement (oracle/oracle_sem.c) and the
+reference's own templates driving it (oracle/_ref RefPmg: pgmres, chebyshev_smooth,
+residual_into, estimate_lambda_max, BandedCholesky).
+
+Bitwise: the operator, its diagonal, the p-transfers, Chebyshev sweeps at a given
+lambda and the Schwarz local solves -- the GPU kernels and the restatement share
+one arithmetic contract (k_sem.cu / oracle_sem.c headers: explicit fma chains,
+no other contraction).
+
+Solves: iteration counts and fine_matvecs exact; solutions within 1e-10
+relative (BASELINE north_star); residual histories entrywise within
+1e-12 * ||r_0|| -- or, on a GMRES plateau, within 10x of the floor two equally
+exact CPU paths show against each other (the restated C drivers vs the
+reference templates, which differ only in the coarse-matrix assembly order).
+The per-entry relative error is printed: it cannot reach 1e-10 at the tail of
+a 1e-8-converged history, because the reference's own sequential dot products
+carry ~1e-14 relative rounding, which enters the iterate and hence the true
+residual at 1e-14 * ||b||, i.e. 1e-6 relative to a 1e-8 * ||b|| residual
+(DESIGN.md §5)."""
 import numpy as np
 import pytest
 import torch
@@ -35,6 +45,28 @@ def rel(a, b):
     return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
 
 
+def same(a, b):
+    """bitwise equality (up to the sign of zero)"""
+    return np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def check_history(h, hr, floor=0.0, what=""):
+    h, hr = np.asarray(h), np.asarray(hr)
+    assert h.size == hr.size
+    d = np.abs(h - hr)
+    per_entry = float(np.max(d / hr))
+    print(f"\n[{what}] history: max|h-h_ref|/h0 = {np.max(d) / hr[0]:.3e}, max per-entry rel = {per_entry:.3e}, "
+          f"CPU-vs-CPU floor/h0 = {floor / hr[0]:.3e}")
+    assert np.max(d) <= max(1e-12 * hr[0], 10.0 * floor)
+    return per_entry
+
+
+def check_x(x, xr, what=""):
+    e = float(np.linalg.norm(x - xr) / np.linalg.norm(xr))
+    print(f"[{what}] x rel err = {e:.3e}")
+    assert e <= TOL
+
+
 @pytest.mark.parametrize("N,ex,ey,ez,geo", [(7, 3, 2, 4, 0), (7, 2, 3, 2, 1), (3, 4, 3, 2, 0), (1, 5, 4, 3, 0),
                                             (5, 2, 2, 3, 1), (2, 3, 3, 3, 0)])
 def test_apply_diag_rhs(sem, N, ex, ey, ez, geo):
@@ -46,9 +78,9 @@ def test_apply_diag_rhs(sem, N, ex, ey, ez, geo):
     y = A.new_vector()
     A.apply(A.from_canonical(x), y)
     assert A.applications() == 1
-    assert rel(A.to_canonical(y), o.apply(x)) <= 1e-12
-    assert rel(A.to_canonical(A.diagonal()), o.diagonal()) <= 1e-12
-    assert rel(A.to_canonical(A.rhs()), o.rhs()) <= 1e-12
+    assert same(A.to_canonical(y), o.apply(x))
+    assert same(A.to_canonical(A.diagonal()), o.diagonal())
+    assert rel(A.to_canonical(A.rhs()), o.rhs()) <= 1e-12  # device sin(): not bitwise
     # padding slots stay exactly zero
     assert torch.all(y.cpu()[torch.from_numpy(~A.valid)] == 0)
 
@@ -70,7 +102,7 @@ def test_sweeps_all_families(cm, sem):
             cm.chebyshev_smooth(A, P.inv_diag(0), cfg, order, A.from_canonical(b), x, xz)
             assert A.applications() == (order - 1 if xz else order)
             ref = o.smooth(0, fam, order, b, np.zeros(o.n[0]) if xz else x0, xz)
-            assert rel(A.to_canonical(x), ref) <= 1e-11, (fam, order, xz)
+            assert same(A.to_canonical(x), ref), (fam, order, xz)
 
 
 def test_transfers_and_coarse_solve(sem):
@@ -82,8 +114,8 @@ def test_transfers_and_coarse_solve(sem):
             xc = ob.random_vector(o.n[l + 1], 5)
             xf = ob.random_vector(o.n[l], 6)
             Pc, Pf = P.ops[l + 1], P.ops[l]
-            assert rel(Pf.to_canonical(P.prolong(l, Pc.from_canonical(xc))), o.prolong(l, xc)) <= 1e-13
-            assert rel(Pc.to_canonical(P.restrict(l, Pf.from_canonical(xf))), o.restrict(l, xf)) <= 1e-13
+            assert same(Pf.to_canonical(P.prolong(l, Pc.from_canonical(xc))), o.prolong(l, xc))
+            assert same(Pc.to_canonical(P.restrict(l, Pf.from_canonical(xf))), o.restrict(l, xf))
         rc = ob.random_vector(o.n[2], 7)
         C1 = P.ops[2]
         assert rel(C1.to_canonical(P.coarse_solve(C1.from_canonical(rc))), o.coarse_solve(rc)) <= 1e-11
@@ -102,26 +134,42 @@ def test_v_cycle(cm, sem, fam, kpre, kpost):
     assert rel(P.A.to_canonical(z), o.v_cycle(fam, kpre, kpost, b)) <= TOL
 
 
+def ref_solve_with_floor(ex, ey, ez, geo, eps, smoother, fam, kpre, kpost, driver=1, floor=True):
+    """The reference-template CPU solve (RefPmg) and, optionally, the floor: the
+    largest history difference between it and the restated C drivers
+    (OraclePmg.solve), an equally exact CPU path."""
+    R = ob.RefPmg((7, 3, 1), ex, ey, ez, geo, eps, smoother=smoother)
+    b = R.sem(0).rhs()
+    ref = R.solve(driver, fam, kpre, kpost, b, tol=1e-8)
+    fl = 0.0
+    if floor:
+        o = ob.OraclePmg((7, 3, 1), ex, ey, ez, geo, eps, smoother=smoother)
+        alt = o.solve(driver, fam, kpre, kpost, b, tol=1e-8)
+        assert (alt.iterations, alt.fine_matvecs) == (ref.iterations, ref.fine_matvecs)
+        fl = float(np.max(np.abs(np.array(alt.history) - np.array(ref.history))))
+    return R, b, ref, fl
+
+
+def gpu_solve(cm, P, fam, kpre, kpost, b, driver=1):
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
+    fn = cm.pgmres if driver == 1 else cm.pcg
+    return fn(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
+
+
 @pytest.mark.parametrize("fam,kpre,kpost,driver", [(2, 4, 0, "pgmres"), (3, 4, 0, "pgmres"), (0, 2, 2, "pgmres"),
                                                    (2, 2, 2, "pcg"), (2, 8, 0, "pgmres")])
 def test_pmg_solves_match_reference_templates(cm, sem, fam, kpre, kpost, driver):
     """p-MG(7,3,1)-preconditioned PGMRES/PCG (tol 1e-8): GPU vs the
-    reference's own pcg/pgmres templates driving the restated SEM operator."""
+    reference's own pcg/pgmres + v_cycle + chebyshev_smooth templates (RefPmg)."""
     ex, ey, ez = 4, 3, 3
-    d = sem.SemDesc(7, ex, ey, ez)
-    P = sem.PMGHierarchy(d, (7, 3, 1))
-    R = ob.ref if ob.ref_available() else None
-    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, lib=R() if R else None)
-    b = o.sem(0).rhs()
     drv = {"pcg": 0, "pgmres": 1}[driver]
-    oref = ob.ref_sem_solve(o, drv, fam, kpre, kpost, b, tol=1e-8) if R else o.solve(drv, fam, kpre, kpost, b)
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
-    fn = cm.pgmres if driver == "pgmres" else cm.pcg
-    x, rep = fn(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
-    assert (rep.iterations, rep.fine_matvecs, rep.status) == (oref.iterations, oref.fine_matvecs, oref.status)
-    h, hr = np.array(rep.residual_history), np.array(oref.history)
-    assert np.max(np.abs(h - hr)) <= TOL * hr[0]
-    assert np.linalg.norm(P.A.to_canonical(x) - oref.x) <= TOL * np.linalg.norm(oref.x)
+    R, b, ref, fl = ref_solve_with_floor(ex, ey, ez, 0, 1.0, 0, fam, kpre, kpost, drv)
+    P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez), (7, 3, 1))
+    assert abs(P.lambda_tilde[0] - R.lambda_tilde[0]) <= 1e-12 * R.lambda_tilde[0]
+    x, rep = gpu_solve(cm, P, fam, kpre, kpost, b, drv)
+    assert (rep.iterations, rep.fine_matvecs, rep.status) == (ref.iterations, ref.fine_matvecs, ref.status)
+    check_history(rep.residual_history, ref.history, fl, f"{driver} {fam} ({kpre},{kpost})")
+    check_x(P.A.to_canonical(x), ref.x)
 
 
 def test_indefinite_level_rejected(sem):
@@ -132,26 +180,20 @@ def test_indefinite_level_rejected(sem):
         sem.PMGHierarchy(sem.SemDesc(7, 36, 36, 9, geometry=sem.KERSHAW, eps=0.05), (7, 3, 1))
 
 
-@pytest.mark.parametrize("eps,kpre,kpost,htol", [(0.3, 4, 0, TOL), (0.3, 8, 0, TOL), (0.5, 4, 0, TOL),
-                                                 (0.5, 2, 2, TOL), (0.3, 2, 2, 1e-6)])
-def test_kershaw_solves(cm, sem, eps, kpre, kpost, htol):
-    """Deformed-mesh config (BASELINE configs[3] shape): half (2k,0) vs full (k,k) cycles.
-    (0.3, (2,2)) needs 86 PGMRES(30) iterations through two restarts; between
-    iterations ~50 and ~70 the history plateaus and 1e-15 differences of the
-    V-cycle (tools/debug_kershaw.py: V-cycle outputs agree to 9e-15) are amplified
-    to ~2e-8 of ||r_0|| before converging again -- iteration counts stay exact."""
+@pytest.mark.parametrize("eps,kpre,kpost", [(0.3, 4, 0), (0.3, 8, 0), (0.5, 4, 0), (0.5, 2, 2), (0.3, 2, 2)])
+def test_kershaw_solves(cm, sem, eps, kpre, kpost):
+    """Deformed-mesh config (BASELINE configs[3] shape): half (2k,0) vs full (k,k)
+    cycles vs the reference templates.  (0.3, (2,2)) needs 86 PGMRES(30)
+    iterations through two restarts and plateaus between iterations ~50 and ~70:
+    there the two CPU paths themselves drift apart by ~1e-9 of ||r_0|| (coarse
+    assembly order only), so the bound is the measured floor, not 1e-12."""
     ex = ey = ez = 3
-    d = sem.SemDesc(7, ex, ey, ez, geometry=sem.KERSHAW, eps=eps)
-    P = sem.PMGHierarchy(d, (7, 3, 1))
-    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, 1, eps)
-    b = o.sem(0).rhs()
-    oref = o.solve(1, 2, kpre, kpost, b, tol=1e-8)
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), kpre, kpost)
-    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
-    assert (rep.iterations, rep.fine_matvecs) == (oref.iterations, oref.fine_matvecs)
-    h, hr = np.array(rep.residual_history), np.array(oref.history)
-    assert np.max(np.abs(h - hr)) <= htol * hr[0]
-    assert np.linalg.norm(P.A.to_canonical(x) - oref.x) <= htol * np.linalg.norm(oref.x)
+    R, b, ref, fl = ref_solve_with_floor(ex, ey, ez, 1, eps, 0, 2, kpre, kpost)
+    P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez, geometry=sem.KERSHAW, eps=eps), (7, 3, 1))
+    x, rep = gpu_solve(cm, P, 2, kpre, kpost, b)
+    assert (rep.iterations, rep.fine_matvecs) == (ref.iterations, ref.fine_matvecs)
+    check_history(rep.residual_history, ref.history, fl, f"kershaw {eps} ({kpre},{kpost})")
+    check_x(P.A.to_canonical(x), ref.x)
 
 
 @pytest.mark.parametrize("ras", [0, 1])
@@ -169,24 +211,24 @@ def test_schwarz_apply(sem, ras, N, geo):
 
     _lib.check(_lib.lib.cmg_pmg_schwarz_apply(P.h, 0, C.c_void_p(P.A.from_canonical(r).data_ptr()),
                                               C.c_void_p(out.data_ptr())))
-    assert rel(P.A.to_canonical(out), o.schwarz(r, ras)) <= 1e-11
+    assert same(P.A.to_canonical(out), o.schwarz(r, ras))
 
 
-@pytest.mark.parametrize("smoother,fam,kpre,kpost", [(2, 2, 2, 0), (1, 2, 2, 0), (2, 0, 1, 1), (1, 3, 2, 0)])
+@pytest.mark.parametrize("smoother,fam,kpre,kpost", [(2, 2, 2, 0), (1, 2, 2, 0), (2, 0, 1, 1), (1, 3, 2, 0),
+                                                     (2, 0, 2, 2), (1, 0, 2, 2), (2, 1, 2, 2)])
 def test_schwarz_pmg_solves(cm, sem, smoother, fam, kpre, kpost):
-    """BASELINE configs[2] shape: Chebyshev-ASM/RAS p-MG(7,3,1) PGMRES (non-symmetric smoother)."""
+    """BASELINE configs[2] shape: Chebyshev-ASM/RAS p-MG(7,3,1) PGMRES (non-symmetric
+    smoother); the 1st-kind (2,2) cases run the fused x += d update of the
+    Schwarz step (EPI_SUPD1 / asm_emit kind 1) at order 2."""
     ex, ey, ez = 3, 3, 2
+    R, b, ref, fl = ref_solve_with_floor(ex, ey, ez, 0, 1.0, smoother, fam, kpre, kpost)
     P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez), (7, 3, 1), smoother=smoother)
-    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, smoother=smoother)
     for l in (0, 1):
-        assert abs(P.lambda_tilde[l] - o.lambda_tilde[l]) <= 1e-10 * o.lambda_tilde[l]
-    b = o.sem(0).rhs()
-    oref = o.solve(1, fam, kpre, kpost, b, tol=1e-8)
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
-    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
-    assert (rep.iterations, rep.fine_matvecs) == (oref.iterations, oref.fine_matvecs)
-    h, hr = np.array(rep.residual_history), np.array(oref.history)
-    assert np.max(np.abs(h - hr)) <= TOL * hr[0]
+        assert abs(P.lambda_tilde[l] - R.lambda_tilde[l]) <= 1e-12 * R.lambda_tilde[l]
+    x, rep = gpu_solve(cm, P, fam, kpre, kpost, b)
+    assert (rep.iterations, rep.fine_matvecs) == (ref.iterations, ref.fine_matvecs)
+    check_history(rep.residual_history, ref.history, fl, f"schwarz {smoother} fam {fam} ({kpre},{kpost})")
+    check_x(P.A.to_canonical(x), ref.x)
 
 
 def test_determinism(cm, sem):
@@ -214,23 +256,21 @@ def config1_pair(sem):
     """BASELINE configs[1] at full size: N=7, E=16^3 (1.37M unknowns), p-MG(7,3,1)."""
     if not ob.ref_available():
         pytest.skip("oracle/_ref not built")
-    o = ob.OraclePmg((7, 3, 1), 16, 16, 16, lib=ob.ref())
+    R = ob.RefPmg((7, 3, 1), 16, 16, 16)
     P = sem.PMGHierarchy(sem.SemDesc(7, 16, 16, 16), (7, 3, 1))
-    return o, P
+    return R, P
 
 
-@pytest.mark.parametrize("fam,kpre,kpost", [(2, 8, 0), (2, 4, 4), (3, 8, 0), (0, 4, 4)])
+@pytest.mark.parametrize("fam,kpre,kpost", [(2, 8, 0), (2, 4, 4), (3, 8, 0), (0, 4, 4), (0, 8, 0), (3, 4, 4)])
 def test_config1_full_size_vs_reference(cm, config1_pair, fam, kpre, kpost):
     """configs[1] (E=16^3) half (2k,0) vs full (k,k) cycles, 1st/4th/opt-4th kind:
-    PGMRES(30) to 1e-8, GPU vs the reference's pgmres template on the restated
-    operator -- same iteration counts, histories and solutions within 1e-10."""
-    o, P = config1_pair
-    assert abs(P.lambda_tilde[0] - o.lambda_tilde[0]) <= 1e-11 * o.lambda_tilde[0]
-    b = o.sem(0).rhs()
-    oref = ob.ref_sem_solve(o, 1, fam, kpre, kpost, b, tol=1e-8)
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(fam), 1, P.lambda_tilde[0]), kpre, kpost)
-    x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8))
-    assert (rep.iterations, rep.fine_matvecs, rep.converged) == (oref.iterations, oref.fine_matvecs, True)
-    h, hr = np.array(rep.residual_history), np.array(oref.history)
-    assert np.max(np.abs(h - hr)) <= TOL * hr[0]
-    assert np.linalg.norm(P.A.to_canonical(x) - oref.x) <= TOL * np.linalg.norm(oref.x)
+    PGMRES(30) to 1e-8, GPU vs the reference templates (RefPmg) -- same iteration
+    counts, histories within 1e-12 ||r_0||, solutions within 1e-10."""
+    R, P = config1_pair
+    assert abs(P.lambda_tilde[0] - R.lambda_tilde[0]) <= 1e-12 * R.lambda_tilde[0]
+    b = R.sem(0).rhs()
+    ref = R.solve(1, fam, kpre, kpost, b, tol=1e-8)
+    x, rep = gpu_solve(cm, P, fam, kpre, kpost, b)
+    assert (rep.iterations, rep.fine_matvecs, rep.converged) == (ref.iterations, ref.fine_matvecs, True)
+    check_history(rep.residual_history, ref.history, 0.0, f"config1 {fam} ({kpre},{kpost})")
+    check_x(P.A.to_canonical(x), ref.x)
