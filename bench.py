@@ -17,6 +17,7 @@ the FD config-1 solve, the roofline and the CPU baseline.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import math
 import os
@@ -123,82 +124,159 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- CPU reference arm
-def cpu_reference_sweep(E: int, order: int, reps: int, seconds_cap: float = 20.0):
-    """Reference chebyshev_smooth template (oracle/_ref, compiled from the reference
-    headers) over the SEM operator restatement; single thread (core.hpp:34-35).
-    Returns (GDOF-step/s, kind, sample description)."""
+def measured_traffic(E, order, world):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the K1/K2 launches of
+    one sweep from the committed ncu --set full capture (tools/ncu_traffic.py ->
+    profiles/r02/sem_sweep_traffic.json), scaled per element to this run's slab."""
+    path = os.path.join(ROOT, "profiles", "r02", "sem_sweep_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+    except Exception:
+        return None
+    scale = (E ** 3 / world) / t["elements"]
+    return {"traffic": t["dram_bytes_per_sweep"] * scale * order / t["order"],
+            "traffic_source": f"ncu --set full, {t['source']}", "traffic_over_algorithmic": t["ratio"]}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def replica_bytes(E: int) -> float:
+    """Host memory of one reference sweep context at E^3 (oracle_sem.c level:
+    G, mass, coordinates, gather map = 88 B per local node; b, x, inv_diag and
+    smooth_fourth's r, d, t + slack = 7 vectors)."""
+    n = (7 * E - 1) ** 3
+    return 88.0 * 512 * E ** 3 + 7 * 8.0 * n
+
+
+def _sweep_replica(E, order, barrier, q):
+    """One reference chebyshev_smooth sweep (oracle/_ref: the reference template over
+    the SEM restatement, single thread) at full size, after every replica's setup."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import ctypes as C
 
-    import numpy as np
-
     import oracle_bind as ob
 
-    use_ref = ob.ref_available()
-    L = ob.ref() if use_ref else ob.oracle()
-    pm = ob.OraclePmg((7, 3, 1), E, E, E, lib=L, eig_iters=30)
-    n = pm.n[0]
-    b = pm.sem(0).rhs()
-    x = ob.random_vector(n, 11)
-    lam = pm.lambda_tilde[0]
-    if use_ref:
-        L.ref_sem_sweep_create.restype = C.c_void_p
-        L.ref_sem_sweep_create.argtypes = [C.c_void_p, C.c_int]
-        L.ref_sem_sweep_run.argtypes = [C.c_void_p, C.c_int, ob.sz, C.c_double, ob.dp, ob.dp, C.c_int, C.c_int]
-        sw = L.ref_sem_sweep_create(pm.p, 0)
-        run = lambda: L.ref_sem_sweep_run(sw, 2, order, lam, ob.P(b), ob.P(x), 0, 1)  # noqa: E731
-        kind = "reference"
-    else:
-        invd = 1.0 / pm.sem(0).diagonal()
-        run = lambda: pm.smooth(0, 2, order, b, x, False, inv_diag=invd)  # noqa: E731
-        kind = "port"
-    run()  # warm
+    L = ob.ref()
+    L.ref_sem_bench_create.restype = C.c_void_p
+    L.ref_sem_bench_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, ob.sz, C.c_uint64]
+    L.ref_sem_bench_n.restype = ob.sz
+    L.ref_sem_bench_n.argtypes = [C.c_void_p]
+    L.ref_sem_bench_sweep.argtypes = [C.c_void_p, C.c_int, ob.sz]
+    L.ref_sem_bench_destroy.argtypes = [C.c_void_p]
     t0 = time.perf_counter()
-    done = 0
-    while done < reps and time.perf_counter() - t0 < seconds_cap:
-        run()
-        done += 1
-    dt = time.perf_counter() - t0
-    sample = (f"SEM N=7 E={E}^3 ({n} unknowns) 4th-kind Chebyshev-Jacobi sweep order {order}, {done} sweeps, "
-              f"{'reference chebyshev_smooth template (oracle/_ref) over the oracle SEM operator' if use_ref else 'oracle port'}")
-    return n * order * done / dt / 1e9, kind, sample
+    h = L.ref_sem_bench_create(7, E, 0, 1.0, 3, 7)
+    setup = time.perf_counter() - t0
+    n = L.ref_sem_bench_n(h) if h else 0
+    if barrier is not None:
+        barrier.wait()
+    t1 = time.perf_counter()
+    rc = L.ref_sem_bench_sweep(h, 2, order) if h else -1
+    dt = time.perf_counter() - t1
+    L.ref_sem_bench_destroy(h)
+    q.put((n, dt, setup, rc))
 
 
-def _replica(args):
-    E, order, reps = args
-    v, kind, sample = cpu_reference_sweep(E, order, reps)
-    return v, kind, sample
+def cpu_reference_sweeps(E: int, order: int, replicas: int):
+    """`replicas` concurrent single-thread reference sweeps at E^3 (one each)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    bar = ctx.Barrier(replicas) if replicas > 1 else None
+    ps = [ctx.Process(target=_sweep_replica, args=(E, order, bar, q)) for _ in range(replicas)]
+    for p in ps:
+        p.start()
+    outs = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    if any(o[3] != 0 for o in outs):
+        raise RuntimeError("reference sweep failed")
+    n = outs[0][0]
+    value = sum(n * order / o[1] for o in outs) / 1e9
+    sample = (f"{replicas} concurrent single-thread replicas x 1 sweep: SEM N=7 E={E}^3 ({n} unknowns) 4th-kind "
+              f"Chebyshev-Jacobi order {order}, reference chebyshev_smooth template (oracle/_ref) over the "
+              f"restated SEM operator; sweep {min(o[1] for o in outs):.1f}-{max(o[1] for o in outs):.1f} s, "
+              f"setup {max(o[2] for o in outs):.0f} s (untimed); CPU: {cpu_model()}")
+    return value, "reference", sample
+
+
+def reference_replicas(E: int) -> int:
+    """All host cores, capped by available host memory (~17 GB per E=64^3 replica)."""
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16e9
+    return max(1, min(cores, int(0.6 * avail / replica_bytes(E))))
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference CPU path on all host cores (independent
-    single-thread replicas, the reference being single-threaded by contract)."""
+    """--impl reference: the reference CPU path on the host cores, same config as
+    the GPU arm (N=7, E^3 = --E), one order-8 sweep per replica (the bounded
+    sample; the reference is single-threaded by contract, core.hpp:34-35, so the
+    cores run independent replicas).  K/W do not apply: one E=64^3 sweep is ~40 s
+    of single-core work."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
-
-    cores = os.cpu_count() or 1
-    E = args.cpu_E
-    order = 8
-    reps = max(1, args.steps)  # timed sweeps per replica (capped at 20 s each)
+    E = args.cpu_E or args.E
+    P = reference_replicas(E)
     t0 = time.perf_counter()
-    with mp.get_context("spawn").Pool(cores) as pool:
-        outs = pool.map(_replica, [(E, order, reps)] * cores)
+    value, kind, sample = cpu_reference_sweeps(E, args.order, P)
     wall = time.perf_counter() - t0
-    value = sum(o[0] for o in outs)
+    n = (7 * E - 1) ** 3
     line = {
         "impl": "reference", "metric": "GDOF/s per Chebyshev smoother sweep", "value": value,
-        "unit": "GDOF-step/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"SEM Poisson box N=7 E={E}^3 4th-kind Chebyshev-Jacobi sweep "
-                                                    f"order 8 (bounded CPU sample of the E=64^3 workload)"},
-        "cpu_baseline": {"value": value, "unit": "GDOF-step/s", "cores": cores, "kind": outs[0][1],
-                         "sample": f"{cores} single-thread replicas x " + outs[0][2]},
+        "unit": "GDOF-step/s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+        "ms_per_step": n * args.order / (value * 1e9) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(E, args.order, n, 1),
+        "cpu_baseline": {"value": value, "unit": "GDOF-step/s", "cores": P, "kind": kind, "sample": sample,
+                         "cpu": cpu_model(), "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "GDOF-step/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
+
+
+def config_of(E, order, n_glob, world):
+    return {"workload": f"SEM Poisson box [-1/2,1/2]^3 N=7 E={E}^3 ({n_glob} unknowns), 4th-kind "
+                        f"Chebyshev-Jacobi sweep order {order} on the fine level of p-MG(7,3,1), warm start",
+            "N": 7, "E": E ** 3, "unknowns": n_glob, "partition": f"z-slabs x{world}",
+            "l2": f"inputs larger than L2 (each vector {n_glob * 8 / world / 1e6:.0f} MB/GPU, G "
+                  f"{6 * 512 * E ** 3 * 8 / world / 1e9:.1f} GB/GPU)"}
+
+
+def fd_reference_run_case():
+    """FD config 1 through the reference's own harness (oracle/_ref run_case_with,
+    harness.hpp:230-258): n=256, factor 2, 4th kind, one-sided k=2 ((4,0)), PGMRES,
+    tol 1e-6; hierarchy built untimed, as on the GPU side."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_bind as ob
+
+    h = ob.RefHierarchy(256, 1.0, 2)
+    best, wall, rep = None, [], None
+    for _ in range(5):
+        t0 = time.perf_counter()
+        rep = h.run_case(2, 2, 1, 1)
+        wall.append(time.perf_counter() - t0)
+    return {"kind": "reference", "run_case_ms": min(wall) * 1e3, "pgmres_ms": rep.wall_time_sec * 1e3,
+            "iterations": rep.iterations, "fine_matvecs": rep.fine_matvecs, "cores": 1, "cpu": cpu_model(),
+            "sample": "reference run_case_with (build_problem + pgmres) on one core, best of 5"}
 
 
 # ---------------------------------------------------------------- BASELINE configs[1..3]
@@ -251,7 +329,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--E", type=int, default=64, help="elements per direction (N=7)")
     ap.add_argument("--order", type=int, default=8)
-    ap.add_argument("--cpu-E", dest="cpu_E", type=int, default=12)
+    ap.add_argument("--cpu-E", dest="cpu_E", type=int, default=0, help="CPU legs' E (default: --E)")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE configs[1..3] solves")
@@ -328,39 +406,72 @@ def main():
     ms_per_step = t_ms / args.steps
     value = n_glob * order * args.steps / (t_ms * 1e-3) / 1e9
 
-    # roofline of the fused step (K1+K2 pair): SURVEY §8(d) algorithmic bytes,
-    # 48 B per local node (6 geometric factors) + 64 B per global unknown
+    # roofline of the fused sweep (K1 + K2 per pass), SURVEY §8(d) algorithmic bytes
+    # per pass: 48 B per local node (6 geometric factors) plus, per global unknown,
+    # 40 B on the residual-initialising pass (gather x; read b, invD; write r, d),
+    # 64 B on a middle step (gather d; read d, x, r, invD; write x, r, d') and 48 B
+    # on the fused last step (no r, d writes): 8*48 N_L + (40 + 6*64 + 48) N_G at order 8
     N_L = 512 * E ** 3
-    bytes_step = 48 * N_L + 64 * n_glob
-    per_gpu_bytes = bytes_step / world
-    step_s = ms_per_step * 1e-3 / order
+    bytes_sweep = order * 48 * N_L + (40 + 64 * (order - 2) + 48) * n_glob
+    per_gpu_bytes = bytes_sweep / world
     peak, peak_src = peaks()
-    achieved = per_gpu_bytes / step_s / 1e9
-    # measured DRAM traffic of the same pair: ncu --set full at E=64^3 (profiles/r01/sem_step_E64_summary.txt),
-    # K1 10.665 GB + K2 2.522 GB per step, scaled per element to this run's slab
-    traffic = (10.665e9 + 2.522e9) / 64 ** 3 * (E ** 3 / world)
+    achieved = per_gpu_bytes / (ms_per_step * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "traffic_source": "ncu dram__bytes_read+write, K1+K2 per step, profiles/r01",
-            "kernel": "fused Chebyshev-Jacobi step (sem K1 element kernel + K2 shared-node kernel)",
-            "algorithmic_bytes_per_step": per_gpu_bytes, "peak_source": peak_src}
+            "traffic": None, "kernel": "fused Chebyshev-Jacobi sweep (sem K1 element kernel + K2 shared-node "
+                                       "kernel, 8 passes)",
+            "algorithmic_bytes_per_sweep": per_gpu_bytes, "peak_source": peak_src}
+    tr = measured_traffic(E, order, world)
+    if tr:
+        roof.update(tr)
 
-    # e2e through the public API with host buffers: every step copies its b, x
-    # in from pinned host memory, sweeps, and copies x out.  Triple-buffered:
-    # step i+1's inputs stream in (copy stream) while step i computes and step
-    # i-1's result streams out (second copy stream), as a solver service would;
-    # a buffer is refilled only after its previous result has been copied out.
-    NB = 3
+    # e2e through the C ABI with host buffers, as a host caller of the library
+    # sees it: every step cmg_upload(b), cmg_upload(x) from
+    # pinned host memory, cmg_chebyshev_smooth, cmg_download(x) -- each copy
+    # synchronous on the context's stream, timed with CUDA events on that stream
+    from paper_2210_03179_b200 import _lib
+
     hb = b.detach().cpu().pin_memory()
     hx = x.detach().cpu().pin_memory()
     hout = torch.empty_like(hx).pin_memory()
+    db, dxv = torch.empty_like(b), torch.empty_like(x)
+    nbytes = b.numel() * 8
+    cc = cfg.c()
+
+    def abi_step():
+        _lib.check(_lib.lib.cmg_upload(ctx.h, C.c_void_p(db.data_ptr()), C.c_void_p(hb.data_ptr()), nbytes))
+        _lib.check(_lib.lib.cmg_upload(ctx.h, C.c_void_p(dxv.data_ptr()), C.c_void_p(hx.data_ptr()), nbytes))
+        _lib.check(_lib.lib.cmg_chebyshev_smooth(A.h, C.c_void_p(invd.data_ptr()), C.byref(cc), order,
+                                                 C.c_void_p(db.data_ptr()), C.c_void_p(dxv.data_ptr()), 0))
+        _lib.check(_lib.lib.cmg_download(ctx.h, C.c_void_p(hout.data_ptr()), C.c_void_p(dxv.data_ptr()), nbytes))
+
+    abi_step()
+    barrier()
+    e2e_steps = max(3, min(args.steps, 8))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        abi_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist:
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e = {"value": n_glob * order / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF-step/s",
+           "h2d_bytes_per_step": 2 * nbytes * world, "d2h_bytes_per_step": nbytes * world, "ms_per_step": e2e_ms,
+           "path": "C ABI cmg_upload x2 + cmg_chebyshev_smooth + cmg_download per step, pinned host buffers"}
+
+    # the same host-buffer workload pipelined the way a solver service would run it:
+    # step i+1's inputs stream in on a copy stream while step i computes and step
+    # i-1's result streams out on a second one (triple-buffered)
+    NB = 3
     bufs = [(b, x)] + [(torch.empty_like(b), torch.empty_like(x)) for _ in range(NB - 1)]
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(NB)]
     ev_done = [torch.cuda.Event() for _ in range(NB)]
     ev_free = [torch.cuda.Event() for _ in range(NB)]
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(NB, min(args.steps, 8))
     e0.record(stream)
     s_in.wait_event(e0)
     for i in range(e2e_steps):
@@ -382,14 +493,14 @@ def main():
     stream.wait_event(ev_free[(e2e_steps - 1) % NB])
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    pipe_ms = e0.elapsed_time(e1) / e2e_steps
     if dist:
-        tt = torch.tensor([e2e_ms], device="cuda")
+        tt = torch.tensor([pipe_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    e2e = {"value": n_glob * order / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF-step/s",
-           "h2d_bytes_per_step": 2 * b.numel() * 8 * world, "d2h_bytes_per_step": x.numel() * 8 * world,
-           "ms_per_step": e2e_ms}
+        pipe_ms = float(tt.item())
+    e2e_pipe = {"value": n_glob * order / (pipe_ms * 1e-3) / 1e9, "unit": "GDOF-step/s", "ms_per_step": pipe_ms,
+                "path": "torch pinned copies on two copy streams around cmg_chebyshev_smooth, triple-buffered"}
+    del bufs
 
     # p-MG(7,3,1)-PGMRES time to solution (tol 1e-8, restart 30), half V-cycle (8,0)
     tts = None
@@ -471,8 +582,10 @@ def main():
         if not args.no_configs:
             configs = baseline_config_solves(cm, sem, ctx, stream)
         if not args.no_cpu:
-            v, kind, sample = cpu_reference_sweep(args.cpu_E, order, reps=50, seconds_cap=15.0)
-            cpu = {"value": v, "unit": "GDOF-step/s", "cores": 1, "kind": kind, "sample": sample}
+            fd["reference_cpu"] = fd_reference_run_case()
+            v, kind, sample = cpu_reference_sweeps(args.cpu_E or E, order, 1)
+            cpu = {"value": v, "unit": "GDOF-step/s", "cores": 1, "kind": kind, "sample": sample,
+                   "cpu": cpu_model(), "host_cores": os.cpu_count()}
 
     if rank == 0:
         line = {
@@ -480,13 +593,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"SEM Poisson box [-1/2,1/2]^3 N=7 E={E}^3 ({n_glob} unknowns), 4th-kind "
-                                   f"Chebyshev-Jacobi sweep order {order} on the fine level of p-MG(7,3,1), "
-                                   f"warm start", "N": 7, "E": E ** 3, "unknowns": n_glob,
-                       "partition": f"z-slabs x{world}", "l2": "inputs larger than L2 (each vector "
-                                                            f"{A.vec_len() * 8 / 1e6:.0f} MB/GPU, G "
-                                                            f"{6 * 512 * E ** 3 * 8 / world / 1e9:.1f} GB/GPU)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "config": config_of(E, order, n_glob, world),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_pipelined": e2e_pipe, "gpu_launches": launches,
             "clocks": clk.summary(), "time_to_solution": tts, "fd_config1": fd, "baseline_configs": configs,
             "setup_s": t_setup, "step_ms_min_max": [min(step_ms), max(step_ms)],
         }

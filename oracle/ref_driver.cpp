@@ -334,6 +334,54 @@ int ref_sem_sweep_run(void* sp, int family, std::size_t order, double lambda_til
   });
 }
 
+// Bench context for the reference CPU arm: ONE SEM level at full size (no
+// hierarchy, no coarse factorisation), b = the PAPER.md RHS, a seeded warm x,
+// inv_diag = jacobi_inverse_diagonal, lambda_tilde from the reference's
+// estimate_lambda_max (setup, untimed; a few iterations suffice for timing).
+struct SemBench {
+  orc_sem* s;
+  SemOperator A;
+  Vec inv_diag, b, x;
+  double lambda;
+};
+
+void* ref_sem_bench_create(int N, int E, int geometry, double eps, std::size_t eig_iters, std::uint64_t seed) {
+  try {
+    orc_sem* s = orc_sem_create(N, E, E, E, geometry, eps);
+    if (!s) throw std::invalid_argument("orc_sem_create failed");
+    SemOperator A(orc_sem_op(s), s);
+    auto* c = new SemBench{s, A, jacobi_inverse_diagonal(A.diagonal()), Vec(A.rows()), random_vector(A.rows(), 11),
+                           0.0};
+    orc_sem_rhs(s, c->b.data());
+    c->lambda = estimate_lambda_max(c->A, c->inv_diag, eig_iters, seed);
+    return c;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+std::size_t ref_sem_bench_n(void* h) { return static_cast<SemBench*>(h)->A.rows(); }
+double ref_sem_bench_lambda(void* h) { return static_cast<SemBench*>(h)->lambda; }
+
+// one warm chebyshev_smooth sweep (smoothers.hpp:156-172) in place on x
+int ref_sem_bench_sweep(void* h, int family, std::size_t order) {
+  auto* c = static_cast<SemBench*>(h);
+  return guarded([&] {
+    ChebyshevConfig cfg;
+    cfg.family = fam(family);
+    cfg.lambda_tilde = c->lambda;
+    chebyshev_smooth(c->A, c->inv_diag, cfg, order, c->b, c->x, false);
+  });
+}
+
+void ref_sem_bench_destroy(void* h) {
+  auto* c = static_cast<SemBench*>(h);
+  if (!c) return;
+  orc_sem_destroy(c->s);
+  delete c;
+}
+
 // p-MG preconditioned PGMRES / PCG through the reference's Krylov templates
 // (krylov.hpp:75-264); the preconditioner is the restated multilevel V-cycle.
 int ref_sem_solve(void* pmg, int driver, int family, double lmax_mult, double lmin_mult,

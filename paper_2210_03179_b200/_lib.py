@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libchebmg_b200.so")
+LIB_PATH = os.environ.get("CMG_LIB") or os.path.join(_HERE, "lib", "libchebmg_b200.so")  # CMG_LIB: A/B builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "chebmg_b200.h")
 
 if not os.path.exists(LIB_PATH):

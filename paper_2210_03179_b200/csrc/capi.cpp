@@ -647,7 +647,6 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
             const cmg_solve_options& o, cmg_solve_report* rep) {
   const double t0 = now_s();
   if (o.restart < 1) fail(CMG_EINVAL, "pgmres: restart must be >= 1");
-  if (o.restart > 63) fail(CMG_EINVAL, "pgmres: restart > 63 not supported");
   cmg_ctx* c = A->ctx;
   cudaStream_t s = c->stream;
   const std::size_t L = A->len;
@@ -675,7 +674,22 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
     finish(A, R, rep, t0);
     return;
   }
-  double* H = dsc + S_H;
+  // scalars of the Arnoldi cycle: the context's fixed slots up to restart 63,
+  // else a workspace sized for m (any restart >= 1, krylov.hpp:148)
+  double *coef = dsc + S_COEF, *coef2 = dsc + S_COEF2, *H = dsc + S_H, *Hs = dsc + S_HS, *g = dsc + S_G,
+         *y = dsc + S_Y, *lsq_work = nullptr;
+  if (m > 63) {
+    const std::size_t nh = static_cast<std::size_t>(m + 1) * m;
+    WBuf sc = wsbuf(c, 8, 2 * (m + 1) + 2 * nh + (m + 1) + m + gmres_lsq_work(m));
+    coef = sc.p;
+    coef2 = coef + (m + 1);
+    H = coef2 + (m + 1);
+    Hs = H + nh;
+    g = Hs + nh;
+    y = g + (m + 1);
+    lsq_work = y + m;
+  }
+  const bool fuse_ok = m <= 63;
   bool done = false;
   while (!done && R.iterations < o.maxit) {
     A->norm2(r.p, dsc + S_BETA);  // beta = norm2(r)
@@ -694,22 +708,22 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
         const char* env = std::getenv("CMG_CGS_FUSE");
         return !(env && std::atoi(env) == 0);
       }();
-      A->mdot(V.p, L, j + 1, w.p, dsc + S_COEF);
-      if (o.reorthogonalize && !fuse_cgs) {
-        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF, w.p, L, H + j, m, s);
-        A->mdot(V.p, L, j + 1, w.p, dsc + S_COEF2);
-        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF2, w.p, L, H + j, m, s);
+      A->mdot(V.p, L, j + 1, w.p, coef);
+      if (o.reorthogonalize && !(fuse_cgs && fuse_ok)) {
+        launch_cgs_update(V.p, L, j + 1, coef, w.p, L, H + j, m, s);
+        A->mdot(V.p, L, j + 1, w.p, coef2);
+        launch_cgs_update(V.p, L, j + 1, coef2, w.p, L, H + j, m, s);
       } else if (o.reorthogonalize) {
-        A->cgs_mdot(V.p, L, j + 1, dsc + S_COEF, w.p, dsc + S_COEF2, H + j, m);
-        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF2, w.p, L, H + j, m, s);
+        A->cgs_mdot(V.p, L, j + 1, coef, w.p, coef2, H + j, m);
+        launch_cgs_update(V.p, L, j + 1, coef2, w.p, L, H + j, m, s);
       } else {
-        launch_cgs_update(V.p, L, j + 1, dsc + S_COEF, w.p, L, H + j, m, s);
+        launch_cgs_update(V.p, L, j + 1, coef, w.p, L, H + j, m, s);
       }
       double* hj1 = H + (std::size_t)(j + 1) * m + j;
       A->norm2(w.p, hj1);
       launch_normalize_if_pos(L, w.p, hj1, V.p + (std::size_t)(j + 1) * L, s);
-      launch_gmres_lsq(H, m, j, 0.0, dsc + S_BETA, dsc + S_HS, dsc + S_G, dsc + S_Y, s);
-      launch_form_iterate(xb.p, Z.p, L, j + 1, dsc + S_Y, xj.p, L, s);
+      launch_gmres_lsq(H, m, j, 0.0, dsc + S_BETA, Hs, g, y, lsq_work, s);
+      launch_form_iterate(xb.p, Z.p, L, j + 1, y, xj.p, L, s);
       A->residual(b, xj.p, rt.p);
       A->norm2(rt.p, dsc + S_RT);
       CMG_CUDA(cudaMemcpyAsync(c->hpin, dsc + S_RT, sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -97,8 +97,9 @@ void launch_cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coe
 void launch_normalize_if_pos(std::size_t n, const double* w, const double* h, double* v,
                              cudaStream_t s);
 // Givens least squares on a copy of H (krylov.hpp:203-227): one thread
-void launch_gmres_lsq(const double* H, int m, int j, double beta_dev_index_unused,
-                      const double* beta_dev, double* Hs, double* g, double* y, cudaStream_t s);
+std::size_t gmres_lsq_work(int m);  // doubles of global workspace for restart m
+void launch_gmres_lsq(const double* H, int m, int j, double, const double* beta_dev, double* Hs, double* g,
+                      double* y, double* gwork, cudaStream_t s);
 // xj = x + sum_l y_l Z_l  (krylov.hpp:228-229)
 void launch_form_iterate(const double* x, const double* Z, std::size_t ldz, int nz,
                          const double* y, double* xj, std::size_t n, cudaStream_t s);

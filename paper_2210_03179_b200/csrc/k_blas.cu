@@ -256,9 +256,14 @@ __global__ void k_normalize_if_pos(std::size_t n, const double* __restrict__ w, 
 // One warp, H staged in shared memory; lane l owns columns l and l+32 of every
 // rotation, so each entry sees exactly the reference's operations in the
 // reference's order (krylov.hpp:203-227) -- only the schedule is parallel.
+// Working copy in dynamic shared memory ((j+2)(j+1) + 2j + 3 doubles), or in
+// `gwork` (global) when that exceeds the shared-memory opt-in (restart > ~165).
 __global__ void k_gmres_lsq(const double* __restrict__ H, int m, int j, const double* beta,
-                            double* Hs, double* g, double* y) {
-  __shared__ double sh[64 * 65], sg[65], sy[64];
+                            double* Hs, double* g, double* y, double* gwork) {
+  extern __shared__ double lsq_smem[];
+  double* sh = gwork ? gwork : lsq_smem;
+  double* sg = sh + (std::size_t)(j + 2) * (j + 1);
+  double* sy = sg + (j + 2);
   const int lane = threadIdx.x;
   const int ld = j + 1;  // columns 0..j
   for (int i = lane; i < (j + 2) * ld; i += 32) sh[i] = H[(i / ld) * m + (i % ld)];
@@ -371,12 +376,16 @@ void launch_finalize(const double* partials, int np, double* out, int do_sqrt, c
 void launch_mdot(const double* V, std::size_t ldv, int nv, const double* w, std::size_t n,
                  double* partials, double* out, cudaStream_t s) {
   const int g = red_grid(n);
-  for (int l0 = 0; l0 < nv; l0 += 16) {
-    k_mdot_partials<16><<<g, kRedThreads, 0, s>>>(V, ldv, nv, l0, w, n, partials);
+  for (int c0 = 0; c0 < nv; c0 += 64) {  // the partials buffer holds 64 vectors; each dot is independent
+    const int nc = nv - c0 < 64 ? nv - c0 : 64;
+    const double* Vc = V + (std::size_t)c0 * ldv;
+    for (int l0 = 0; l0 < nc; l0 += 16) {
+      k_mdot_partials<16><<<g, kRedThreads, 0, s>>>(Vc, ldv, nc, l0, w, n, partials);
+      CMG_LAUNCH_CHECK();
+    }
+    k_finalize<<<nc, kRedThreads, 0, s>>>(partials, g, out + c0, 0, nc);
     CMG_LAUNCH_CHECK();
   }
-  k_finalize<<<nv, kRedThreads, 0, s>>>(partials, g, out, 0, nv);
-  CMG_LAUNCH_CHECK();
 }
 
 void launch_axpy(std::size_t n, double alpha, const double* x, double* y, cudaStream_t s) {
@@ -451,8 +460,12 @@ void launch_any_nonzero(std::size_t n, const double* d, int* flag, cudaStream_t 
 
 void launch_cgs_update(const double* V, std::size_t ldv, int nv, const double* coef, double* w,
                        std::size_t n, double* hcol, int hstride, cudaStream_t s) {
-  k_cgs_update<<<vgrid(n), 256, 0, s>>>(V, ldv, nv, coef, w, n, hcol, hstride);
-  CMG_LAUNCH_CHECK();
+  for (int l0 = 0; l0 < nv; l0 += 64) {  // chunks continue each entry's sequential axpy order
+    const int nc = nv - l0 < 64 ? nv - l0 : 64;
+    k_cgs_update<<<vgrid(n), 256, 0, s>>>(V + (std::size_t)l0 * ldv, ldv, nc, coef + l0, w, n,
+                                          hcol + (std::size_t)l0 * hstride, hstride);
+    CMG_LAUNCH_CHECK();
+  }
 }
 void launch_cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coef, double* w, std::size_t n,
                     double* hcol, int hstride, double* partials, double* out, cudaStream_t s) {
@@ -469,15 +482,31 @@ void launch_normalize_if_pos(std::size_t n, const double* w, const double* h, do
   k_normalize_if_pos<<<vgrid(n), 256, 0, s>>>(n, w, h, v);
   CMG_LAUNCH_CHECK();
 }
+std::size_t gmres_lsq_work(int m) { return (std::size_t)(m + 1) * m + 2 * (std::size_t)m + 1; }
+
 void launch_gmres_lsq(const double* H, int m, int j, double, const double* beta_dev, double* Hs,
-                      double* g, double* y, cudaStream_t s) {
-  k_gmres_lsq<<<1, 32, 0, s>>>(H, m, j, beta_dev, Hs, g, y);
+                      double* g, double* y, double* gwork, cudaStream_t s) {
+  constexpr std::size_t kMaxSmem = 227 * 1024;
+  static bool configured = false;
+  if (!configured) {
+    CMG_CUDA(cudaFuncSetAttribute(k_gmres_lsq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+    configured = true;
+  }
+  const std::size_t bytes = gmres_lsq_work(j + 1) * sizeof(double);
+  if (bytes <= kMaxSmem) k_gmres_lsq<<<1, 32, bytes, s>>>(H, m, j, beta_dev, Hs, g, y, nullptr);
+  else k_gmres_lsq<<<1, 32, 0, s>>>(H, m, j, beta_dev, Hs, g, y, gwork);
   CMG_LAUNCH_CHECK();
 }
+// xj = x + sum_l y_l Z_l, per entry in ascending l; more than 64 columns run as
+// consecutive chunks continuing from the stored partial sum (same operations,
+// same order, same bits)
 void launch_form_iterate(const double* x, const double* Z, std::size_t ldz, int nz,
                          const double* y, double* xj, std::size_t n, cudaStream_t s) {
-  k_form_iterate<<<vgrid(n), 256, 0, s>>>(x, Z, ldz, nz, y, xj, n);
-  CMG_LAUNCH_CHECK();
+  for (int l0 = 0; l0 < nz || l0 == 0; l0 += 64) {
+    const int nc = nz - l0 < 64 ? nz - l0 : 64;
+    k_form_iterate<<<vgrid(n), 256, 0, s>>>(l0 == 0 ? x : xj, Z + (std::size_t)l0 * ldz, ldz, nc, y + l0, xj, n);
+    CMG_LAUNCH_CHECK();
+  }
 }
 void launch_pcg_alpha(const double* rz, const double* pAp, double* alpha, int* stop_flag,
                       cudaStream_t s) {

@@ -729,7 +729,8 @@ struct SemLevel final : cmg_op {
   void dot(const double* a, const double* b, double* out) override { layer_reduce(a, 0, 1, b, out, false); }
   void norm2(const double* a, double* out) override { layer_reduce(a, 0, 1, a, out, true); }
   void mdot(const double* V, std::size_t ldv, int nv, const double* w, double* out) override {
-    layer_reduce(V, ldv, nv, w, out, false);
+    for (int c0 = 0; c0 < nv; c0 += 64)  // each inner product is reduced independently
+      layer_reduce(V + static_cast<std::size_t>(c0) * ldv, ldv, std::min(64, nv - c0), w, out + c0, false);
   }
   void cgs_mdot(const double* V, std::size_t ldv, int nv, const double* coef_in, double* w, double* out,
                 double* hcol, int hstride) override {

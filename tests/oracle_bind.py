@@ -574,3 +574,48 @@ class RefPmg:
         assert rc == 0, self.R.ref_last_error()
         return Report(its.value, mv.value, hist[: hl.value].tolist(), bool(cv.value), st.value.decode(), rho.value,
                       wall_time_sec=wall.value, x=x)
+
+
+# ---------------------------------------------------------------- reference-side binding
+ADAPTER_SO = os.path.join(ROOT, "oracle", "_ref", "libchebmg_adapter.so")
+_ad = None
+
+
+def adapter_available() -> bool:
+    return os.path.exists(ADAPTER_SO)
+
+
+def adapter():
+    """oracle/_ref/libchebmg_adapter.so: integration/chebmg_b200_adapter.hpp compiled
+    against the unmodified reference headers (oracle/adapter_driver.cpp entry points)."""
+    global _ad
+    if _ad is None:
+        L = C.CDLL(ADAPTER_SO)
+        out = [dp, sz, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz), C.POINTER(C.c_int), C.c_char_p]
+        L.ad_last_error.restype = C.c_char_p
+        L.ad_fd_smooth.argtypes = [sz, C.c_double, C.c_int, sz, C.c_double, dp, dp, C.c_int, C.POINTER(sz)]
+        L.ad_fd_solve_templates.argtypes = [sz, C.c_double, sz, C.c_int, sz, sz, C.c_int, C.c_double, dp] + out
+        L.ad_fd_run_case_b200.argtypes = [sz, C.c_double, sz, C.c_int, sz, C.c_int, C.c_int, C.c_double] + out + [
+            C.POINTER(C.c_double)]
+        L.ad_pmg_create.restype = C.c_void_p
+        L.ad_pmg_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int]
+        L.ad_pmg_destroy.argtypes = [C.c_void_p]
+        L.ad_pmg_lambda.restype = C.c_double
+        L.ad_pmg_lambda.argtypes = [C.c_void_p, C.c_int]
+        L.ad_pmg_smooth.argtypes = [C.c_void_p, C.c_int, sz, C.c_double, dp, dp, C.c_int, C.POINTER(sz)]
+        L.ad_pmg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, sz, sz, dp, C.c_double, dp] + out
+        _ad = L
+    return _ad
+
+
+def adapter_report(fn, *args, maxit=500, n=0, extra=()):
+    """Call an adapter solve entry point (trailing outputs: hist, cap, len, its, mv, cv, status)."""
+    x = np.zeros(n)
+    hist = np.zeros(maxit + 2)
+    hl, its, mv = sz(), sz(), sz()
+    cv = C.c_int()
+    st = C.create_string_buffer(128)
+    head = list(args) + ([P(x)] if n else [])
+    rc = fn(*head, P(hist), maxit + 2, C.byref(hl), C.byref(its), C.byref(mv), C.byref(cv), st, *extra)
+    assert rc == 0, adapter().ad_last_error()
+    return Report(its.value, mv.value, hist[: hl.value].tolist(), bool(cv.value), st.value.decode(), x=x)

@@ -332,3 +332,27 @@ def test_sweep_csv_matches_reference_sweep(cm, tmp_path):
                              for r, b in zip(sr.rows, ref)])
     cm.select_best_rows(ref_sr)
     assert ref_sr.best_per_group == sr.best_per_group
+
+
+@pytest.mark.parametrize("restart", [30, 63, 64, 70, 100, 200])
+def test_pgmres_any_restart_matches_reference(cm, restart):
+    """krylov.hpp:148 accepts any restart >= 1: above 63 the Arnoldi scalars move to a
+    restart-sized workspace, the least-squares solve to dynamic shared (or global)
+    memory and the multi-dots / updates / iterate run in 64-vector chunks with the
+    same per-entry order.  84 PGMRES iterations (n=128, Lx=64, 1st kind k=1),
+    so restarts 30..70 restart and 100/200 do not -- vs the compiled reference."""
+    n, Lx, f = 128, 64.0, 2
+    ref = ob.RefHierarchy(n, Lx, f).run_case(0, 1, 1, 1, restart=restart)
+    cfg = cm.CaseConfig(Lx=Lx, n=n, factor=f, family=cm.Family.first, k=1, cycle=cm.Cycle.one_sided,
+                        driver=cm.Driver.pgmres, restart=restart)
+    r = cm.run_case(cfg)
+    assert (r.report.iterations, r.report.fine_matvecs, r.report.status) == (ref.iterations, ref.fine_matvecs,
+                                                                             ref.status)
+    h, hr = np.array(r.report.residual_history), np.array(ref.history)
+    assert np.max(np.abs(h - hr) / hr) <= TOL_REL
+
+
+def test_pgmres_restart_zero_rejected(cm):
+    cfg = cm.CaseConfig(n=32, driver=cm.Driver.pgmres, restart=0)
+    with pytest.raises(ValueError, match="restart must be >= 1"):
+        cm.run_case(cfg)

@@ -32,6 +32,11 @@ VARIANTS = [
 
 @pytest.mark.parametrize("var,val,path,sel", VARIANTS, ids=[f"{v}={x}:{os.path.basename(p)}" for v, x, p, _ in VARIANTS])
 def test_variant_parity(var, val, path, sel):
+    if "multigpu" in path:
+        import torch
+
+        if torch.cuda.device_count() < 2:
+            pytest.skip("the multi-GPU parity tests need >= 2 GPUs (they would all skip in the child)")
     env = dict(os.environ, **{var: val})
     r = subprocess.run([sys.executable, "-m", "pytest", path, "-m", "gpu", "-q", "-x", "-k", sel, "-p", "no:cacheprovider"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)

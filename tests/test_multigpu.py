@@ -1,5 +1,5 @@
 """Multi-GPU element partition (BASELINE configs[4] shape): the same p-MG(7,3,1)
-PGMRES solve at 1, 2 (and 4) GPUs must give BITWISE identical residual
+PGMRES solve at 1, 2 (4, 8) GPUs must give BITWISE identical residual
 histories and solutions -- the gather-scatter sums and the inner products are
 reduced in a fixed global order -- and the 1-GPU run matches
 the oracle (tests/test_sem_gpu.py).  Needs >= 2 GPUs (gpurun --gpus 2)."""
@@ -23,6 +23,10 @@ def _ngpus():
         return 0
 
 
+def _worlds():
+    return [w for w in (2, 4, 8) if _ngpus() >= w]
+
+
 def _run(world, out, extra=()):
     script = os.path.join(ROOT, "tools", "mgpu_check.py")
     if world == 1:
@@ -40,11 +44,10 @@ def _run(world, out, extra=()):
 def test_partition_bitwise_identical(tmp_path, geometry):
     extra = ("--geometry", str(geometry))
     r1 = _run(1, str(tmp_path / "r1.json"), extra)
-    worlds = [2] + ([4] if _ngpus() >= 4 else [])
     import numpy as np
 
     x1 = np.load(str(tmp_path / "r1.json") + ".x.npy")
-    for w in worlds:
+    for w in _worlds():
         rw = _run(w, str(tmp_path / f"r{w}.json"), extra)
         for k in ("iterations", "fine_matvecs", "history", "lambda"):
             assert rw[k] == r1[k], (w, k)
@@ -66,11 +69,35 @@ def test_schwarz_partition_bitwise_identical(tmp_path, smoother, geometry):
     extra = ("--smoother", str(smoother), "--geometry", str(geometry), "--kpre", "2")
     r1 = _run(1, str(tmp_path / "s1.json"), extra)
     x1 = np.load(str(tmp_path / "s1.json") + ".x.npy")
-    for w in [2] + ([4] if _ngpus() >= 4 else []):
+    for w in _worlds():
         rw = _run(w, str(tmp_path / f"s{w}.json"), extra)
         for k in ("iterations", "fine_matvecs", "history", "lambda"):
             assert rw[k] == r1[k], (w, k)
         xw = np.load(str(tmp_path / f"s{w}.json") + ".x.npy")
+        assert np.array_equal(xw, x1), (w, np.max(np.abs(xw - x1)))
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("smoother,family,kpre,kpost", [(0, 2, 4, 0), (2, 2, 2, 0), (1, 2, 2, 0), (2, 0, 2, 2),
+                                                        (1, 0, 2, 2)],
+                         ids=["jacobi", "ras", "asm", "ras-1st-2-2", "asm-1st-2-2"])
+def test_one_layer_per_rank_bitwise_identical(tmp_path, smoother, family, kpre, kpost):
+    """Ez = world: every rank holds ONE element layer (Ezl = 1), so the first and
+    the last owned layer coincide -- the face halo, the bottom-face contribution
+    return, the Schwarz ghost planes from both neighbours and the ASM box sums
+    all touch the same layer.  Bitwise the 1-GPU solve of the same mesh; the
+    1st-kind (2,2) Schwarz cases run the fused x += d update at order 2."""
+    import numpy as np
+
+    for w in _worlds():
+        extra = ("--ez", str(w), "--smoother", str(smoother), "--family", str(family), "--kpre", str(kpre),
+                 "--kpost", str(kpost))
+        r1 = _run(1, str(tmp_path / f"o1_{w}.json"), extra)
+        rw = _run(w, str(tmp_path / f"o{w}.json"), extra)
+        for k in ("iterations", "fine_matvecs", "history", "lambda"):
+            assert rw[k] == r1[k], (w, k)
+        x1 = np.load(str(tmp_path / f"o1_{w}.json") + ".x.npy")
+        xw = np.load(str(tmp_path / f"o{w}.json") + ".x.npy")
         assert np.array_equal(xw, x1), (w, np.max(np.abs(xw - x1)))
 
 
@@ -101,7 +128,7 @@ def test_full_size_partition_identity(tmp_path):
     extra = ("--E", "64", "--ez", "64", "--kpre", "8", "--hash-only")
     r1 = _run(1, str(tmp_path / "f1.json"), extra)
     assert r1["iterations"] == 9
-    for w in [2] + ([4] if _ngpus() >= 4 else []):
+    for w in _worlds():
         rw = _run(w, str(tmp_path / f"f{w}.json"), extra)
         for k in ("iterations", "fine_matvecs", "history", "lambda", "x_sha256"):
             assert rw[k] == r1[k], (w, k)

@@ -1,5 +1,5 @@
 """Multi-rank host logic of the element-partitioned SEM path, on CPU with the
-gloo backend (world_size 2 and 4).  Each rank builds its z-slab maps through the
+gloo backend (world_size 2, 4 and 8; at 8 every rank holds one element layer, Ezl = 1).  Each rank builds its z-slab maps through the
 C-ABI host entry points; the ranks exchange them with torch.distributed and
 check that (1) every canonical unknown is owned by exactly one (rank, slot),
 (2) the input-face halo a rank receives (the top c=N-1 owned layer of the rank
@@ -118,7 +118,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_slab_partition_halo_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

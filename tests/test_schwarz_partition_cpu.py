@@ -18,7 +18,7 @@ def owner(g, N, ne):
 
 
 @pytest.mark.parametrize("N", [2, 3, 4, 5, 7])
-@pytest.mark.parametrize("Ez,nranks", [(8, 2), (8, 4), (6, 3), (4, 4)])
+@pytest.mark.parametrize("Ez,nranks", [(8, 2), (8, 4), (6, 3), (4, 4), (8, 8), (16, 8)])
 def test_box_reads_cross_one_layer_in_fixed_planes(N, Ez, nranks):
     for rank in range(nranks):
         z0, z1 = rank * Ez // nranks, (rank + 1) * Ez // nranks
@@ -43,7 +43,7 @@ def test_box_reads_cross_one_layer_in_fixed_planes(N, Ez, nranks):
 
 
 @pytest.mark.parametrize("N", [2, 3, 4, 5, 7])
-@pytest.mark.parametrize("Ez,nranks", [(8, 2), (8, 4), (6, 3), (4, 4)])
+@pytest.mark.parametrize("Ez,nranks", [(8, 2), (8, 4), (6, 3), (4, 4), (8, 8), (16, 8)])
 def test_asm_sum_visits_fixed_neighbour_box_planes(N, Ez, nranks):
     for rank in range(nranks):
         z0, z1 = rank * Ez // nranks, (rank + 1) * Ez // nranks

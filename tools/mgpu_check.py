@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--hash-only", action="store_true", help="write a sha256 of x instead of x itself")
     ap.add_argument("--kpre", type=int, default=4)
+    ap.add_argument("--kpost", type=int, default=0)
+    ap.add_argument("--family", type=int, default=2, help="0 first, 1 first_opt_lambda, 2 fourth, 3 fourth_opt")
     ap.add_argument("--smoother", type=int, default=0, help="0 Jacobi, 1 ASM, 2 RAS (Chebyshev-Schwarz)")
     args = ap.parse_args()
     import numpy as np
@@ -51,7 +53,7 @@ def main():
     d = sem.SemDesc(7, args.E, args.E, args.ez, geometry=args.geometry, eps=0.3, rank=rank, nranks=world)
     P = sem.PMGHierarchy(d, (7, 3, 1), smoother=args.smoother, ctx=ctx)
     b = P.A.rhs()
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), args.kpre, 0)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family(args.family), 1, P.lambda_tilde[0]), args.kpre, args.kpost)
     x, rep = cm.pgmres(P.A, P.preconditioner(cyc), b, None, cm.SolveOptions(tol=1e-8))
     # gather the canonical solution on rank 0
     xc = P.A.to_canonical(x)
