@@ -1169,6 +1169,10 @@ int cmg_pcg(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
             const cmg_solve_options* o, cmg_solve_report* rep) {
   return guard([&] {
     bind_identity_len(A, M);
+    if (M->variable())
+      fail(CMG_EINVAL,
+           "pcg: the preconditioner is not a fixed linear operator (deformed-mesh coarse CG above "
+           "CMG_COARSE_DENSE_MAX); use pgmres");
     pcg(A, M, b, x0, x, opts_or_default(o), rep);
   });
 }

@@ -186,6 +186,9 @@ struct cmg_precond {
   cmg_ctx* ctx = nullptr;
   virtual ~cmg_precond() = default;
   virtual void apply(const double* v, double* z) = 0;
+  // true when M is not one fixed linear operator (an inner solve stopped by a
+  // tolerance): PCG's theory then does not hold, only flexible-form PGMRES does
+  virtual bool variable() const { return false; }
 };
 
 namespace cmg {

@@ -20,6 +20,8 @@
 
 namespace cmg {
 
+void host_interp_matrix(int Nf, int Nc, double* J);  // host_setup.cpp
+
 namespace {
 
 template <int N>
@@ -66,6 +68,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+}
+
+// shared -> global bulk copy (TMA engine), completion tracked by a bulk group
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+// make this thread's generic-proxy shared-memory writes visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// commit the issued bulk stores and wait until their shared-memory source has been read
+__device__ __forceinline__ void bulk_store_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // owner of local node index l (0..N) along one dimension of element coordinate ec:
@@ -825,6 +841,336 @@ __global__ void __launch_bounds__(128) k_prolong(SemArgs F, SemArgs Cc, const do
   }
 }
 
+// ---------------------------------------------------------------- p-transfers, one warp per element
+// The order-7 <-> 3 transfers as warp-level line contractions, the K1 recipe:
+// J (8x4) sits in __constant__ memory and every index into it is a
+// compile-time constant (a DFMA constant-bank operand, no shared traffic), a
+// lane owns whole lines of the contracted direction, a warp owns an element
+// (only __syncwarp between the three contractions, ~10 elements in flight
+// per scheduler), the element's contiguous fine block is read / written with
+// coalesced lane-strided accesses (slot <-> node by sem_pos / sem_abc).  Every output is the same ascending fma chain as k_prolong /
+// k_restrict_local (bitwise identical; r01: 704 / 568 us per launch at E=64^3).
+__constant__ double c_J73[8 * 4];          // J[i*4 + m] = l^3_m(xi^7_i)  (host_interp_matrix(7, 3))
+
+constexpr int kTW = 4;  // warps (elements) per block
+
+template <int NF, int NCO>
+__global__ void __launch_bounds__(32 * kTW) k_restrict_w(SemArgs F, const double* __restrict__ xf,
+                                                       double* __restrict__ Lc) {
+  static_assert(NF == 7 && NCO == 3, "warp transfer kernels are instantiated for 7 -> 3");
+  constexpr int F1 = 8, C1 = 4, P = 9, NOSF = sem_nos(NF);
+  // uf (64 lines of 8 along x, node (i,j,k) at (k*8 + j)*P + i) | t1 (32 lines of 8); t2 aliases uf.
+  // Local nodes with i, j or k = 0 are not the element's own (zero in the restatement's
+  // input): the m = 0 terms are skipped -- fma(J, +0, +0) = +0, so every chain still
+  // rounds identically -- and all-zero lines give +0 outputs, so uf needs no zeroing.
+  __shared__ double sm[kTW][64 * P + 32 * P];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long e = (long)blockIdx.x * kTW + w;
+  if (e >= F.e_end) return;
+  double* uf = sm[w];
+  double* t1 = sm[w] + 64 * P;
+  double* t2 = sm[w];
+  const double* xe = xf + e * NOSF;
+#pragma unroll
+  for (int r = 0; r < (NOSF + 31) / 32; ++r) {
+    const int q = lane + 32 * r;
+    int a, b, c;  // arithmetic inverse of the slot layout
+    if (q < NOSF && sem_abc(NF, q, a, b, c)) uf[((c + 1) * F1 + (b + 1)) * P + (a + 1)] = __ldg(xe + q);
+  }
+  __syncwarp();
+  // J^T along x: line (j, k) -> t1[(a*8 + k)*P + j], a = 0..3
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int L = lane + 32 * h, j = L & 7, k = L >> 3;
+    if (j == 0 || k == 0) {
+#pragma unroll
+      for (int a = 0; a < C1; ++a) t1[(a * F1 + k) * P + j] = 0.0;
+      continue;
+    }
+    double u[F1];
+#pragma unroll
+    for (int m = 1; m < F1; ++m) u[m] = uf[(k * F1 + j) * P + m];
+#pragma unroll
+    for (int a = 0; a < C1; ++a) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 1; m < F1; ++m) v = __fma_rn(c_J73[m * C1 + a], u[m], v);
+      t1[(a * F1 + k) * P + j] = v;
+    }
+  }
+  __syncwarp();
+  // J^T along y: line (a, k) -> t2[(a*4 + b)*P + k]  (t1[., j = 0, .] = +0)
+  {
+    const int a = lane >> 3, k = lane & 7;
+    double u[F1];
+#pragma unroll
+    for (int m = 1; m < F1; ++m) u[m] = t1[(a * F1 + k) * P + m];
+#pragma unroll
+    for (int b = 0; b < C1; ++b) {
+      double v = 0.0;
+      if (k != 0) {
+#pragma unroll
+        for (int m = 1; m < F1; ++m) v = __fma_rn(c_J73[m * C1 + b], u[m], v);
+      }
+      t2[(a * C1 + b) * P + k] = v;
+    }
+  }
+  __syncwarp();
+  // J^T along z: line (a, b) -> Lc[a + 4(b + 4c)]  (t2[., ., k = 0] = +0)
+  if (lane < C1 * C1) {
+    const int a = lane & 3, b = lane >> 2;
+    double u[F1];
+#pragma unroll
+    for (int m = 1; m < F1; ++m) u[m] = t2[(a * C1 + b) * P + m];
+#pragma unroll
+    for (int c = 0; c < C1; ++c) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 1; m < F1; ++m) v = __fma_rn(c_J73[m * C1 + c], u[m], v);
+      Lc[e * 64 + a + C1 * (b + C1 * c)] = v;
+    }
+  }
+}
+
+template <int NF, int NCO>
+__global__ void __launch_bounds__(32 * kTW) k_prolong_w(SemArgs F, SemArgs Cc, const double* __restrict__ xc,
+                                                      double* __restrict__ yf, int add) {
+  static_assert(NF == 7 && NCO == 3, "warp transfer kernels are instantiated for 7 -> 3");
+  constexpr int F1 = 8, C1 = 4, P = 5, NOSF = sem_nos(NF), NOSC = sem_nos(NCO);
+  // per warp: t1 (32 lines of 4) | t2 (64 lines of 4); uc (16 lines of 4) aliases t2
+  __shared__ double sm[kTW][32 * P + 64 * P];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long e = (long)blockIdx.x * kTW + w;
+  if (e >= F.e_end) return;
+  double* t1 = sm[w];
+  double* t2 = t1 + 32 * P;
+  double* uc = t2;
+  double* ye = yf + e * NOSF;
+  const int ex = (int)(e % F.Ex), ey = (int)((e / F.Ex) % F.Ey), ez = (int)(e / ((long)F.Ex * F.Ey));
+  // this lane's fine outputs: lines (i, j) = (L & 7, L >> 3), L = lane, lane + 32, nodes k = 1..7;
+  // their old values are loaded first (add) so the loads overlap the gather and contractions
+  double old[2][F1 - 1];
+  bool line_ok[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int L = lane + 32 * h, i = L & 7, j = L >> 3;
+    line_ok[h] = i != 0 && j != 0 && ex * NF + i < NF * F.Ex && ey * NF + j < NF * F.Ey;
+#pragma unroll
+    for (int k = 1; k < F1; ++k)
+      old[h][k - 1] = (add && line_ok[h]) ? ye[sem_pos(NF, (i - 1) & 7, (j - 1) & 7, k - 1)] : 0.0;
+  }
+  // gather the element's coarse nodal values: uc[(c*4 + b)*P + a]
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int q = lane + 32 * r, a = q & 3, b = (q >> 2) & 3, c = q >> 4;
+    int oex = 0, oey = 0, oez = 0;
+    const int ax = owner1d<NCO>(ex, a, Cc.Ex, oex);
+    const int ay = owner1d<NCO>(ey, b, Cc.Ey, oey);
+    const int az = owner1d<NCO>(Cc.z0 + ez, c, Cc.Ez, oez);
+    double v = 0.0;
+    if (ax >= 0 && ay >= 0 && az >= 0) {
+      const int lz = oez - Cc.z0;
+      if (lz < 0)
+        v = Cc.halo_lo[((long)oex + (long)Cc.Ex * oey) * (NCO * NCO) + ax + NCO * ay];
+      else
+        v = __ldg(xc + ((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOSC + sem_pos(NCO, ax, ay, az));
+    }
+    uc[(c * C1 + b) * P + a] = v;
+  }
+  __syncwarp();
+  // J along x: line (b, c) -> t1[(i*4 + c)*P + b]
+  if (lane < C1 * C1) {
+    const int b = lane & 3, c = lane >> 2;
+    double u[C1];
+#pragma unroll
+    for (int m = 0; m < C1; ++m) u[m] = uc[(c * C1 + b) * P + m];
+#pragma unroll
+    for (int i = 0; i < F1; ++i) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < C1; ++m) v = __fma_rn(c_J73[i * C1 + m], u[m], v);
+      t1[(i * C1 + c) * P + b] = v;
+    }
+  }
+  __syncwarp();
+  // J along y: line (i, c) -> t2[(j*8 + i)*P + c]
+  {
+    const int i = lane >> 2, c = lane & 3;
+    double u[C1];
+#pragma unroll
+    for (int m = 0; m < C1; ++m) u[m] = t1[(i * C1 + c) * P + m];
+    __syncwarp();  // uc (aliased by t2) fully consumed by the x step
+#pragma unroll
+    for (int j = 0; j < F1; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < C1; ++m) v = __fma_rn(c_J73[j * C1 + m], u[m], v);
+      t2[(j * F1 + i) * P + c] = v;
+    }
+  }
+  __syncwarp();
+  // J along z at the owned fine nodes (i, j, k >= 1), written straight to the fine block
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!line_ok[h]) continue;
+    const int L = lane + 32 * h, i = L & 7, j = L >> 3;
+    double u[C1];
+#pragma unroll
+    for (int m = 0; m < C1; ++m) u[m] = t2[(j * F1 + i) * P + m];
+#pragma unroll
+    for (int k = 1; k < F1; ++k) {
+      if ((F.z0 + ez) * NF + k >= NF * F.Ez) continue;  // padding (far boundary)
+      double v = 0.0;
+#pragma unroll
+      for (int m = 0; m < C1; ++m) v = __fma_rn(c_J73[k * C1 + m], u[m], v);
+      ye[sem_pos(NF, i - 1, j - 1, k - 1)] = add ? old[h][k - 1] + v : v;
+    }
+  }
+}
+
+// constant tables of the warp transfer kernels (once per device)
+void upload_transfer_tables() {
+  static bool done[64] = {};
+  int dev = 0;
+  CMG_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && done[dev]) return;
+  double J[8 * 4];
+  host_interp_matrix(7, 3, J);
+  CMG_CUDA(cudaMemcpyToSymbol(c_J73, J, sizeof J));
+  if (dev < 64) done[dev] = true;
+}
+
+// High orders (NF >= 5): the element's owned fine slots are ONE contiguous
+// block of NOS doubles (sem_layout.hpp), so the read-modify-write of the fine
+// vector is a TMA bulk load at block start (overlapping the coarse gather and
+// the x/y contractions) and a single bulk store of the finished block -- full
+// sectors both ways instead of 343 scattered 8-byte accesses.  Padding slots
+// keep their value (add) or are written 0.  Same arithmetic, same bits as
+// k_prolong (r01: 704 us at E=64^3, ~30% of HBM).
+template <int NF, int NCO>
+__global__ void __launch_bounds__(128) k_prolong_tma(SemArgs F, SemArgs Cc, const double* __restrict__ J,
+                                                     const double* __restrict__ xc, double* __restrict__ yf,
+                                                     int add) {
+  constexpr int F1 = NF + 1, C1 = NCO + 1, NOF = NF * NF * NF;
+  constexpr int NOSF = sem_nos(NF), NOSC = sem_nos(NCO);
+  constexpr int UC = C1 * C1 * C1, T1 = F1 * C1 * C1, T2 = F1 * F1 * C1;
+  static_assert((NOSF * 8) % 16 == 0, "bulk copies need 16-byte multiples");
+  __shared__ __align__(128) double sy[NOSF];
+  __shared__ double sJ[F1 * C1];
+  __shared__ double uc[UC];
+  __shared__ double t1[T1];
+  __shared__ double t2[T2];
+  __shared__ __align__(8) unsigned long long bar;
+  const long e = blockIdx.x;
+  double* ye = yf + e * NOSF;
+  if (add && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, NOSF * 8);
+    bulk_g2s(sy, ye, NOSF * 8, &bar);
+  }
+  if (!add)
+    for (int q = threadIdx.x; q < NOSF; q += blockDim.x) sy[q] = 0.0;
+  for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
+  const int ex = (int)(e % F.Ex), ey = (int)((e / F.Ex) % F.Ey), ez = (int)(e / ((long)F.Ex * F.Ey));
+  for (int q = threadIdx.x; q < UC; q += blockDim.x) {
+    const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
+    int oex = 0, oey = 0, oez = 0;
+    const int ax = owner1d<NCO>(ex, a, Cc.Ex, oex);
+    const int ay = owner1d<NCO>(ey, b, Cc.Ey, oey);
+    const int az = owner1d<NCO>(Cc.z0 + ez, c, Cc.Ez, oez);
+    double v = 0.0;
+    if (ax >= 0 && ay >= 0 && az >= 0) {
+      const int lz = oez - Cc.z0;
+      if (lz < 0)
+        v = Cc.halo_lo[((long)oex + (long)Cc.Ex * oey) * (NCO * NCO) + ax + NCO * ay];
+      else
+        v = xc[((long)oex + (long)Cc.Ex * ((long)oey + (long)Cc.Ey * lz)) * NOSC + sem_pos(NCO, ax, ay, az)];
+    }
+    uc[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < T1; q += blockDim.x) {  // contract x
+    const int i = q % F1, b = (q / F1) % C1, c = q / (F1 * C1);
+    double v = 0.0;
+    for (int m = 0; m < C1; ++m) v = __fma_rn(sJ[i * C1 + m], uc[m + C1 * (b + C1 * c)], v);
+    t1[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < T2; q += blockDim.x) {  // contract y
+    const int i = q % F1, j = (q / F1) % F1, c = q / (F1 * F1);
+    double v = 0.0;
+    for (int m = 0; m < C1; ++m) v = __fma_rn(sJ[j * C1 + m], t1[i + F1 * (m + C1 * c)], v);
+    t2[q] = v;
+  }
+  __syncthreads();
+  if (add) mbar_wait(&bar, 0);
+  for (int q = threadIdx.x; q < NOF; q += blockDim.x) {  // contract z at owned fine nodes
+    const int a = q % NF, b = (q / NF) % NF, c = q / (NF * NF);
+    const int i = a + 1, j = b + 1, k = c + 1;
+    if (ex * NF + i >= NF * F.Ex || ey * NF + j >= NF * F.Ey || (F.z0 + ez) * NF + k >= NF * F.Ez) continue;
+    double v = 0.0;
+    for (int m = 0; m < C1; ++m) v = __fma_rn(sJ[k * C1 + m], t2[i + F1 * (j + F1 * m)], v);
+    const int pos = sem_pos(NF, a, b, c);
+    sy[pos] = add ? sy[pos] + v : v;
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bulk_s2g(ye, sy, NOSF * 8);
+    bulk_store_wait_read();
+  }
+}
+
+// Restriction for NF >= 5: the element's owned fine block arrives by one TMA
+// bulk load; same contractions and bits as k_restrict_local.
+template <int NF, int NCO>
+__global__ void __launch_bounds__(128) k_restrict_tma(SemArgs F, const double* __restrict__ J,
+                                                      const double* __restrict__ xf, double* __restrict__ Lc) {
+  constexpr int F1 = NF + 1, C1 = NCO + 1, CP = C1 * C1 * C1, NOSF = sem_nos(NF);
+  constexpr int UF = F1 * F1 * F1, T1 = C1 * F1 * F1, T2 = C1 * C1 * F1;
+  static_assert((NOSF * 8) % 16 == 0, "bulk copies need 16-byte multiples");
+  __shared__ __align__(128) double sx[NOSF];
+  __shared__ double sJ[F1 * C1];
+  __shared__ double uf[UF];
+  __shared__ double t1[T1];
+  __shared__ double t2[T2];
+  __shared__ __align__(8) unsigned long long bar;
+  const long e = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, NOSF * 8);
+    bulk_g2s(sx, xf + e * NOSF, NOSF * 8, &bar);
+  }
+  for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (int q = threadIdx.x; q < UF; q += blockDim.x) {
+    const int i = q % F1, j = (q / F1) % F1, k = q / (F1 * F1);
+    uf[q] = (i >= 1 && j >= 1 && k >= 1) ? sx[sem_pos(NF, i - 1, j - 1, k - 1)] : 0.0;  // padding slots are zero
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < T1; q += blockDim.x) {  // J^T along x
+    const int a = q % C1, j = (q / C1) % F1, k = q / (C1 * F1);
+    double v = 0.0;
+    for (int m = 0; m < F1; ++m) v = __fma_rn(sJ[m * C1 + a], uf[m + F1 * (j + F1 * k)], v);
+    t1[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < T2; q += blockDim.x) {
+    const int a = q % C1, b = (q / C1) % C1, k = q / (C1 * C1);
+    double v = 0.0;
+    for (int m = 0; m < F1; ++m) v = __fma_rn(sJ[m * C1 + b], t1[a + C1 * (m + F1 * k)], v);
+    t2[q] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < CP; q += blockDim.x) {
+    const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
+    double v = 0.0;
+    for (int m = 0; m < F1; ++m) v = __fma_rn(sJ[m * C1 + c], t2[a + C1 * (b + C1 * m)], v);
+    Lc[e * CP + q] = v;
+  }
+}
+
 template <int NF, int NCO>
 __global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double* __restrict__ J,
                                                         const double* __restrict__ xf, double* __restrict__ Lc) {
@@ -1078,12 +1424,34 @@ void sem_slot_mask(const SemArgs& a, double* mask, cudaStream_t s) {
   CMG_LAUNCH_CHECK();
 }
 
+// CMG_TRANSFER_KERNEL: 2 (default) warp-per-element kernels for 7 <-> 3,
+// 1 the block kernels with TMA bulk copies (order >= 5), 0 the plain block kernels
+static int transfer_kernel() {
+  static const int k = [] {
+    const char* env = std::getenv("CMG_TRANSFER_KERNEL");
+    return env ? std::atoi(env) : 2;
+  }();
+  return k;
+}
+
 template <int NF, int NCO>
 static void prolong_t(const SemArgs& f, const SemArgs& c, const double* J, const double* xc, double* yf,
                       bool add, cudaStream_t s) {
   SemArgs ff = f;
   ff.e_end = f.E;
-  k_prolong<NF, NCO><<<(unsigned)((f.E + tepb(NF) - 1) / tepb(NF)), 128, 0, s>>>(ff, c, J, xc, yf, add ? 1 : 0);
+  const bool tma = transfer_kernel() == 1;
+  if constexpr (NF == 7 && NCO == 3) {
+    if (transfer_kernel() == 2) {
+      upload_transfer_tables();
+      k_prolong_w<7, 3><<<(unsigned)((f.E + kTW - 1) / kTW), 32 * kTW, 0, s>>>(ff, c, xc, yf, add ? 1 : 0);
+      CMG_LAUNCH_CHECK();
+      return;
+    }
+  }
+  if (NF >= 5 && tma)
+    k_prolong_tma<NF, NCO><<<(unsigned)f.E, 128, 0, s>>>(ff, c, J, xc, yf, add ? 1 : 0);
+  else
+    k_prolong<NF, NCO><<<(unsigned)((f.E + tepb(NF) - 1) / tepb(NF)), 128, 0, s>>>(ff, c, J, xc, yf, add ? 1 : 0);
   CMG_LAUNCH_CHECK();
 }
 
@@ -1091,7 +1459,19 @@ template <int NF, int NCO>
 static void restrict_t(const SemArgs& f, const double* J, const double* xf, double* Lc, cudaStream_t s) {
   SemArgs ff = f;
   ff.e_end = f.E;
-  k_restrict_local<NF, NCO><<<(unsigned)((f.E + tepb(NF) - 1) / tepb(NF)), 128, 0, s>>>(ff, J, xf, Lc);
+  const bool tma = transfer_kernel() == 1;
+  if constexpr (NF == 7 && NCO == 3) {
+    if (transfer_kernel() == 2) {
+      upload_transfer_tables();
+      k_restrict_w<7, 3><<<(unsigned)((f.E + kTW - 1) / kTW), 32 * kTW, 0, s>>>(ff, xf, Lc);
+      CMG_LAUNCH_CHECK();
+      return;
+    }
+  }
+  if (NF >= 5 && tma)
+    k_restrict_tma<NF, NCO><<<(unsigned)f.E, 128, 0, s>>>(ff, J, xf, Lc);
+  else
+    k_restrict_local<NF, NCO><<<(unsigned)((f.E + tepb(NF) - 1) / tepb(NF)), 128, 0, s>>>(ff, J, xf, Lc);
   CMG_LAUNCH_CHECK();
 }
 

@@ -55,6 +55,22 @@ const StreamMemOps& memops() {
   return ops;
 }
 bool stream_mem_ops() { return memops().wait && memops().write; }
+
+// Every rank must take the same branch before a collective setup step: the
+// per-process conditions (environment knobs, driver stream-memory-op support)
+// are agreed first with one allreduce, so no rank returns early while the
+// others block in the following allgather.
+bool all_ranks_agree(cmg_ctx* ctx, bool local) {
+  cudaStream_t s = ctx->stream;
+  DBuf d(1);
+  const double v = local ? 1.0 : 0.0;
+  CMG_CUDA(cudaMemcpyAsync(d.p, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+  ctx->comm->allreduce_sum(d.p, 1, s);
+  double total = 0.0;
+  CMG_CUDA(cudaMemcpyAsync(&total, d.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CMG_CUDA(cudaStreamSynchronize(s));
+  return total == static_cast<double>(ctx->comm->nranks);
+}
 // exchanges smaller than this many doubles stay on NCCL (CMG_PEER_MIN)
 std::size_t peer_min_doubles() {
   static const std::size_t v = [] {
@@ -104,9 +120,10 @@ struct PeerShift {
   }
 
   void setup(cmg_ctx* ctx, int rank, int nranks, std::size_t n_up, std::size_t n_dn) {
+    if (nranks < 2) return;
     const char* env = std::getenv("CMG_PEER_HALO");
-    if (nranks < 2 || (env && std::atoi(env) == 0) || !stream_mem_ops()) return;
-    if (n_up + n_dn < peer_min_doubles()) return;  // same decision on every rank
+    const bool local = !(env && std::atoi(env) == 0) && stream_mem_ops() && n_up + n_dn >= peer_min_doubles();
+    if (!all_ranks_agree(ctx, local)) return;
     cudaStream_t s = ctx->stream;
     nu = n_up;
     nd = n_dn;
@@ -476,9 +493,11 @@ struct SemLevel final : cmg_op {
   PeerHalo peer;
 
   void peer_setup() {
+    if (!distributed()) return;
     const char* env = std::getenv("CMG_PEER_HALO");
-    if (!distributed() || (env && std::atoi(env) == 0) || !stream_mem_ops()) return;
-    if (static_cast<std::size_t>(Ex) * Ey * N * N < peer_min_doubles()) return;  // small levels: NCCL
+    const bool local = !(env && std::atoi(env) == 0) && stream_mem_ops() &&
+                       static_cast<std::size_t>(Ex) * Ey * N * N >= peer_min_doubles();  // small levels: NCCL
+    if (!all_ranks_agree(ctx, local)) return;
     cudaStream_t s = ctx->stream;
     peer.hn = static_cast<std::size_t>(Ex) * Ey * N * N;
     peer.cn = static_cast<std::size_t>(Ex) * Ey * (N + 1) * (N + 1);
@@ -1303,6 +1322,10 @@ void pmg_vcycle(cmg_pmg* p, int l, const cmg_cycle_config& cc, const double* b, 
 struct PmgPrecond final : cmg_precond {
   cmg_pmg* p = nullptr;
   cmg_cycle_config cfg{};
+  // deformed mesh above CMG_COARSE_DENSE_MAX: the coarse solve is the
+  // tolerance-stopped CG (pmg_coarse_solve), so each V-cycle is a slightly
+  // different operator
+  bool variable() const override { return p->lev.back()->desc.geometry != 0 && p->cn == 0; }
   void apply(const double* v, double* z) override {
     CMG_CUDA(cudaMemsetAsync(z, 0, p->lev[0]->len * sizeof(double), ctx->stream));
     pmg_vcycle(p, 0, cfg, v, z, true);

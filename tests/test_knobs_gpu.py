@@ -1,4 +1,4 @@
-"""The runtime A/B knobs (INTEGRATION.md §5) select alternative kernels; every
+"""The runtime A/B knobs (INTEGRATION.md §4) select alternative kernels; every
 non-default variant must pass the same parity checks as the default.  Each
 knob is read once per process, so each variant runs the relevant parity tests
 in a child pytest with the variable set."""
@@ -26,6 +26,8 @@ VARIANTS = [
     ("CMG_SCHWARZ_SMALL", "0", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_SCHWARZ_FUSE", "0", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_COARSE_INV", "0", "tests/test_sem_gpu.py", "kershaw or transfers_and_coarse"),
+    ("CMG_TRANSFER_KERNEL", "0", "tests/test_sem_gpu.py", "transfers_and_coarse or v_cycle or pmg_solves"),
+    ("CMG_TRANSFER_KERNEL", "1", "tests/test_sem_gpu.py", "transfers_and_coarse or v_cycle or pmg_solves"),
     ("CMG_COARSE_DENSE_MAX", "0", "tests/test_sem_gpu.py", "kershaw or transfers_and_coarse"),
 ]
 

@@ -61,10 +61,11 @@ def check_history(h, hr, floor=0.0, what=""):
     return per_entry
 
 
-def check_x(x, xr, what=""):
+def check_x(x, xr, what="", floor=0.0):
+    """x within 1e-10 relative, or within 10x a measured CPU-vs-CPU floor (relative)"""
     e = float(np.linalg.norm(x - xr) / np.linalg.norm(xr))
-    print(f"[{what}] x rel err = {e:.3e}")
-    assert e <= TOL
+    print(f"[{what}] x rel err = {e:.3e} (CPU-vs-CPU floor {floor:.3e})")
+    assert e <= max(TOL, 10.0 * floor)
 
 
 @pytest.mark.parametrize("N,ex,ey,ez,geo", [(7, 3, 2, 4, 0), (7, 2, 3, 2, 1), (3, 4, 3, 2, 0), (1, 5, 4, 3, 0),
@@ -284,17 +285,41 @@ def test_config1_full_size_vs_reference(cm, config1_pair, fam, kpre, kpost):
 @pytest.mark.parametrize("restart", [70, 120])
 def test_sem_pgmres_restart_above_63(cm, sem, restart):
     """restart > 63 on the SEM path (layer multi-dots in 64-vector chunks): the
-    86-iteration Kershaw (2,2) solve without (120) and with (70) a restart."""
+    111-iteration Kershaw eps=0.3 (2,0) solve with one restart (70) and none
+    (120).  A weak smoother on a deformed mesh stalls on GMRES plateaus, where
+    the two exact CPU paths already differ by ~1e-6 ||r0|| in the history and
+    ~3e-10 in x, so both bounds are 10x that measured floor."""
     ex = ey = ez = 3
     R = ob.RefPmg((7, 3, 1), ex, ey, ez, 1, 0.3)
     b = R.sem(0).rhs()
-    ref = R.solve(1, 2, 2, 2, b, tol=1e-8, restart=restart)
-    alt = ob.OraclePmg((7, 3, 1), ex, ey, ez, 1, 0.3).solve(1, 2, 2, 2, b, tol=1e-8, restart=restart)
+    ref = R.solve(1, 2, 2, 0, b, tol=1e-8, restart=restart)
+    alt = ob.OraclePmg((7, 3, 1), ex, ey, ez, 1, 0.3).solve(1, 2, 2, 0, b, tol=1e-8, restart=restart)
     floor = float(np.max(np.abs(np.array(alt.history) - np.array(ref.history))))
+    floor_x = float(np.linalg.norm(alt.x - ref.x) / np.linalg.norm(ref.x))
     P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez, geometry=sem.KERSHAW, eps=0.3), (7, 3, 1))
-    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 2, 2)
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 2, 0)
     x, rep = cm.pgmres(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None,
                        cm.SolveOptions(tol=1e-8, restart=restart))
+    assert rep.iterations > 64
     assert (rep.iterations, rep.fine_matvecs, rep.status) == (ref.iterations, ref.fine_matvecs, ref.status)
     check_history(rep.residual_history, ref.history, floor, f"restart {restart}")
+    check_x(P.A.to_canonical(x), ref.x, f"restart {restart}", floor_x)
+
+
+def test_coarse_cg_fallback_under_pgmres_and_pcg_rejected(cm, sem, monkeypatch):
+    """Deformed mesh above CMG_COARSE_DENSE_MAX (forced to 0 here): the p=1 solve is
+    the tolerance-stopped CG (relative residual 1e-13), a variable preconditioner.
+    PGMRES still reproduces the reference template's iteration count and
+    solution; PCG refuses it (EINVAL) instead of running without its theory."""
+    monkeypatch.setenv("CMG_COARSE_DENSE_MAX", "0")
+    ex = ey = ez = 3
+    R, b, ref, _ = ref_solve_with_floor(ex, ey, ez, 1, 0.3, 0, 2, 4, 0, floor=False)
+    P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez, geometry=sem.KERSHAW, eps=0.3), (7, 3, 1))
+    x, rep = gpu_solve(cm, P, 2, 4, 0, b)
+    assert (rep.iterations, rep.fine_matvecs) == (ref.iterations, ref.fine_matvecs)
+    h, hr = np.array(rep.residual_history), np.array(ref.history)
+    print(f"\n[coarse CG] max|h-h_ref|/h0 = {np.max(np.abs(h - hr)) / hr[0]:.3e}")
+    assert np.max(np.abs(h - hr)) <= 1e-10 * hr[0]
     check_x(P.A.to_canonical(x), ref.x)
+    with pytest.raises(ValueError, match="not a fixed linear operator"):
+        gpu_solve(cm, P, 2, 2, 2, b, driver=0)
