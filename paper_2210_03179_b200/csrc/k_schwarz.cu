@@ -197,6 +197,99 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   }
 }
 
+// Same local solve with the contraction loops interchanged: a thread streams
+// the eigenbasis ROW m (S[m][0..PB) forward, the row of a transposed copy
+// backward, both broadcast as 16-byte loads) against the m-th value of its two
+// lines and keeps all 2*PB accumulators live, so 2*PB independent fma chains
+// are in flight instead of 4 (k_schwarz_local is latency-bound: one DFMA
+// chain of PB terms per output pair).  Each output is still one fma chain over
+// ascending m: bitwise identical to k_schwarz_local and the restatement.
+template <int N>
+__global__ void __launch_bounds__(64) k_schwarz_local_il(SchwarzArgs A) {
+  constexpr int PB = N + 3, PB2 = PB * PB, PB3 = PB2 * PB, N1 = N + 1;
+  static_assert(PB % 2 == 0, "interchanged loops read eigenbasis rows in pairs");
+  constexpr int PX = PB | 1, PS = PX * PB;
+  __shared__ double u[PS * PB], t[PS * PB];
+  __shared__ __align__(16) double S[3][PB2];   // S[d][m*PB + o]: forward  out[o] += S[m][o] in[m]
+  __shared__ __align__(16) double ST[3][PB2];  // ST[d][m*PB + o] = S[d][o*PB + m]: backward
+  __shared__ double lam[3][PB];
+  const long e = blockIdx.x;
+  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+  for (int d = 0; d < 3; ++d) {
+    const int id = A.sidx[e * 3 + d];
+    for (int q = threadIdx.x; q < PB2; q += blockDim.x) {
+      const double v = A.S[(long)id * PB2 + q];
+      S[d][q] = v;
+      ST[d][(q % PB) * PB + q / PB] = v;
+    }
+    for (int q = threadIdx.x; q < PB; q += blockDim.x) lam[d][q] = A.lam[(long)id * PB + q];
+  }
+  for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
+    const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
+    u[a + PX * b + PS * c] = box_value<N>(A, ex, ey, ez, a, b, c);
+  }
+  __syncthreads();
+  constexpr int HALF = (PB2 + 1) / 2;
+  double* in = u;
+  double* out = t;
+#pragma unroll 1
+  for (int pass = 0; pass < 6; ++pass) {
+    const int dim = pass % 3;
+    const double* Sd = pass < 3 ? S[dim] : ST[dim];
+    const int st = dim == 0 ? 1 : (dim == 1 ? PX : PS);
+    for (int l = threadIdx.x; l < HALF; l += blockDim.x) {
+      const int l2 = l + HALF;
+      const bool two = l2 < PB2;
+      const int p1 = l % PB, q1 = l / PB, p2 = (two ? l2 : l) % PB, q2 = (two ? l2 : l) / PB;
+      const int b1 = dim == 0 ? PX * p1 + PS * q1 : (dim == 1 ? p1 + PS * q1 : p1 + PX * q1);
+      const int b2 = dim == 0 ? PX * p2 + PS * q2 : (dim == 1 ? p2 + PS * q2 : p2 + PX * q2);
+      double a[PB], c[PB];
+#pragma unroll
+      for (int o = 0; o < PB; ++o) a[o] = c[o] = 0.0;
+#pragma unroll 1
+      for (int m = 0; m < PB; ++m) {  // not unrolled: keeps the 2*PB accumulators, not 5*PB loads, live
+        const double v1 = in[b1 + m * st], v2 = in[b2 + m * st];
+#pragma unroll
+        for (int o = 0; o < PB; o += 2) {
+          const double2 sp = *reinterpret_cast<const double2*>(Sd + m * PB + o);
+          a[o] = __fma_rn(sp.x, v1, a[o]);
+          a[o + 1] = __fma_rn(sp.y, v1, a[o + 1]);
+          c[o] = __fma_rn(sp.x, v2, c[o]);
+          c[o + 1] = __fma_rn(sp.y, v2, c[o + 1]);
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < PB; ++o) {
+        out[b1 + o * st] = a[o];
+        if (two) out[b2 + o * st] = c[o];
+      }
+    }
+    __syncthreads();
+    if (pass == 2) {  // the eigenvalue division as its own elementwise sweep (a division's slow
+                      // path is a call: kept away from the 2*PB live accumulators)
+      for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
+        const int x = q % PB, y = (q / PB) % PB, z = q / PB2;
+        out[x + PX * y + PS * z] /= (lam[0][x] + lam[1][y] + lam[2][z]);
+      }
+      __syncthreads();
+    }
+    double* tmp = in;
+    in = out;
+    out = tmp;
+  }
+  if (A.ras) {
+    for (int q = threadIdx.x; q < N1 * N1 * N1; q += blockDim.x) {
+      const int i = q % N1, j = (q / N1) % N1, k = q / (N1 * N1);
+      A.Lout[e * (N1 * N1 * N1) + q] = in[(i + 1) + PX * (j + 1) + PS * (k + 1)];
+    }
+  } else {
+    for (int q = threadIdx.x; q < PB3; q += blockDim.x) {
+      const int a = q % PB, b = (q / PB) % PB, c = q / PB2;
+      A.Lout[e * PB3 + q] = in[a + PX * b + PS * c];
+    }
+  }
+}
+
 // Low orders (N <= 4, the p=3 level of the (7,3,1) Schwarz schedule): a box
 // has only (N+3)^2 <= 49 lines per pass, so one element per block left most
 // threads idle.  EPB elements share a block, one line per thread; every
@@ -512,6 +605,11 @@ void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
     const char* env = std::getenv("CMG_SCHWARZ_MMA");
     return env && std::atoi(env) == 1;
   }();
+  // interchanged-loop local solve (CMG_SCHWARZ_IL=0 keeps k_schwarz_local)
+  static const bool il = [] {
+    const char* env = std::getenv("CMG_SCHWARZ_IL");
+    return !(env && std::atoi(env) == 0);
+  }();
   // low orders: several elements per block (CMG_SCHWARZ_SMALL=0 keeps one per block)
   static const bool small = [] {
     const char* env = std::getenv("CMG_SCHWARZ_SMALL");
@@ -528,6 +626,7 @@ void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
 #define X(n)                                                                  \
   if (a.N == n) {                                                             \
     if (use_mma) k_schwarz_local_mma<n><<<(unsigned)E, 128, 0, s>>>(a);      \
+    else if (il && (n + 3) % 2 == 0) k_schwarz_local_il<(n + 3) % 2 == 0 ? n : 5><<<(unsigned)E, 64, 0, s>>>(a); \
     else k_schwarz_local<n><<<(unsigned)E, 64, 0, s>>>(a);                    \
     CMG_LAUNCH_CHECK();                                                       \
     return;                                                                   \
