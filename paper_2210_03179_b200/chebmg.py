@@ -198,7 +198,7 @@ class StencilOperator(DeviceOperator):
         self._own = True
 
     def __del__(self):
-        if getattr(self, "_own", False):
+        if getattr(self, "_own", False) and lib is not None:  # lib is None at interpreter shutdown
             lib.cmg_op_destroy(self.h)
 
 
@@ -355,7 +355,7 @@ class Hierarchy:
         return ec
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib.cmg_fd_hierarchy_destroy(self.h)
             self.h = None
 
@@ -449,7 +449,7 @@ class Preconditioner:
         return z
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib.cmg_precond_destroy(self.h)
             self.h = None
 

@@ -605,10 +605,13 @@ void sem_schwarz_local(const SchwarzArgs& a, cudaStream_t s) {
     const char* env = std::getenv("CMG_SCHWARZ_MMA");
     return env && std::atoi(env) == 1;
   }();
-  // interchanged-loop local solve (CMG_SCHWARZ_IL=0 keeps k_schwarz_local)
+  // interchanged-loop local solve, opt-in (CMG_SCHWARZ_IL=1): measured 636 vs
+  // 570 us per apply at E=32^3 and RAS (1,1) 23.8 vs 23.0 ms (profiles/r02/
+  // schwarz_il_ab.txt) -- 96 registers, so fewer resident blocks, and the
+  // per-m row loads are no cheaper than the per-output ones they replace
   static const bool il = [] {
     const char* env = std::getenv("CMG_SCHWARZ_IL");
-    return !(env && std::atoi(env) == 0);
+    return env && std::atoi(env) == 1;
   }();
   // low orders: several elements per block (CMG_SCHWARZ_SMALL=0 keeps one per block)
   static const bool small = [] {

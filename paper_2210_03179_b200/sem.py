@@ -139,7 +139,7 @@ class SemOperator(DeviceOperator, _Layout):
         return b
 
     def __del__(self):
-        if getattr(self, "_own", False):
+        if getattr(self, "_own", False) and lib is not None:  # lib is None at interpreter shutdown
             lib.cmg_op_destroy(self.h)
 
 
@@ -207,6 +207,6 @@ class PMGHierarchy:
         return Preconditioner(p, keep=self)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib.cmg_pmg_destroy(self.h)
             self.h = None

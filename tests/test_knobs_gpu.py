@@ -24,7 +24,7 @@ VARIANTS = [
     ("CMG_FD_GRAPHS", "0", "tests/test_fd_gpu.py", "golden_solves or preconditioner_cost"),
     ("CMG_SCHWARZ_MMA", "1", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_SCHWARZ_SMALL", "0", "tests/test_sem_gpu.py", "schwarz"),
-    ("CMG_SCHWARZ_IL", "0", "tests/test_sem_gpu.py", "schwarz"),
+    ("CMG_SCHWARZ_IL", "1", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_SCHWARZ_FUSE", "0", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_COARSE_INV", "0", "tests/test_sem_gpu.py", "kershaw or transfers_and_coarse"),
     ("CMG_TRANSFER_KERNEL", "0", "tests/test_sem_gpu.py", "transfers_and_coarse or v_cycle or pmg_solves"),
