@@ -254,11 +254,13 @@ def run_reference_arm(args):
 
 
 def config_of(E, order, n_glob, world):
+    """The workload -- identical for the GPU arm at any N and the reference arm
+    (the partition is reported next to it, not in it)."""
     return {"workload": f"SEM Poisson box [-1/2,1/2]^3 N=7 E={E}^3 ({n_glob} unknowns), 4th-kind "
                         f"Chebyshev-Jacobi sweep order {order} on the fine level of p-MG(7,3,1), warm start",
-            "N": 7, "E": E ** 3, "unknowns": n_glob, "partition": f"z-slabs x{world}",
-            "l2": f"inputs larger than L2 (each vector {n_glob * 8 / world / 1e6:.0f} MB/GPU, G "
-                  f"{6 * 512 * E ** 3 * 8 / world / 1e9:.1f} GB/GPU)"}
+            "N": 7, "E": E ** 3, "unknowns": n_glob,
+            "l2": f"inputs larger than L2 (each vector {n_glob * 8 / 1e6:.0f} MB, geometric factors "
+                  f"{6 * 512 * E ** 3 * 8 / 1e9:.1f} GB in total)"}
 
 
 def fd_reference_run_case():
@@ -593,7 +595,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": config_of(E, order, n_glob, world),
+            "config": config_of(E, order, n_glob, world), "partition": f"element z-slabs x{world}",
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_pipelined": e2e_pipe, "gpu_launches": launches,
             "clocks": clk.summary(), "time_to_solution": tts, "fd_config1": fd, "baseline_configs": configs,
             "setup_s": t_setup, "step_ms_min_max": [min(step_ms), max(step_ms)],

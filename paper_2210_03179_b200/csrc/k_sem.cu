@@ -863,13 +863,15 @@ __global__ void __launch_bounds__(32 * kTW) k_restrict_w(SemArgs F, const double
   // Local nodes with i, j or k = 0 are not the element's own (zero in the restatement's
   // input): the m = 0 terms are skipped -- fma(J, +0, +0) = +0, so every chain still
   // rounds identically -- and all-zero lines give +0 outputs, so uf needs no zeroing.
-  __shared__ double sm[kTW][64 * P + 32 * P];
+  // one 64-line buffer per warp: uf, then t1 (lines 0..31) and t2 (lines 32..47) once the
+  // x step has pulled its two uf lines into registers (18 KB per block, 12 blocks per SM)
+  __shared__ double sm[kTW][64 * P];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long e = (long)blockIdx.x * kTW + w;
   if (e >= F.e_end) return;
   double* uf = sm[w];
-  double* t1 = sm[w] + 64 * P;
-  double* t2 = sm[w];
+  double* t1 = sm[w];
+  double* t2 = sm[w] + 32 * P;
   const double* xe = xf + e * NOSF;
 #pragma unroll
   for (int r = 0; r < (NOSF + 31) / 32; ++r) {
@@ -879,22 +881,25 @@ __global__ void __launch_bounds__(32 * kTW) k_restrict_w(SemArgs F, const double
   }
   __syncwarp();
   // J^T along x: line (j, k) -> t1[(a*8 + k)*P + j], a = 0..3
+  double u2[2][F1];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int L = lane + 32 * h, j = L & 7, k = L >> 3;
-    if (j == 0 || k == 0) {
 #pragma unroll
-      for (int a = 0; a < C1; ++a) t1[(a * F1 + k) * P + j] = 0.0;
-      continue;
-    }
-    double u[F1];
+    for (int m = 1; m < F1; ++m) u2[h][m] = (j == 0 || k == 0) ? 0.0 : uf[(k * F1 + j) * P + m];
+  }
+  __syncwarp();  // uf fully read: t1 / t2 reuse its storage
 #pragma unroll
-    for (int m = 1; m < F1; ++m) u[m] = uf[(k * F1 + j) * P + m];
+  for (int h = 0; h < 2; ++h) {
+    const int L = lane + 32 * h, j = L & 7, k = L >> 3;
+    const bool zero = j == 0 || k == 0;
 #pragma unroll
     for (int a = 0; a < C1; ++a) {
       double v = 0.0;
+      if (!zero) {
 #pragma unroll
-      for (int m = 1; m < F1; ++m) v = __fma_rn(c_J73[m * C1 + a], u[m], v);
+        for (int m = 1; m < F1; ++m) v = __fma_rn(c_J73[m * C1 + a], u2[h][m], v);
+      }
       t1[(a * F1 + k) * P + j] = v;
     }
   }
