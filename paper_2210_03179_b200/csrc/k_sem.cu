@@ -84,6 +84,21 @@ __device__ __forceinline__ void bulk_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// Block-wide wait until *flag >= v (a peer GPU's stream memop writes the epoch after
+// its producing kernel; acquire at system scope, then the CTA barrier orders every
+// thread's later reads of the peer buffer after it).  Called by all threads.
+__device__ __forceinline__ void block_wait_flag(const unsigned* flag, unsigned v) {
+  if (threadIdx.x == 0) {
+    unsigned x;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(flag) : "memory");
+      if ((int)(x - v) >= 0) break;
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
+
 // owner of local node index l (0..N) along one dimension of element coordinate ec:
 // returns the owned-slot coordinate in the owner (oe) or -1 for a Dirichlet node
 template <int N>
@@ -395,7 +410,7 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
         // halo: k=0 face of the layer above, indexed by (ex', ey', i', j')
         const int dx = f & 1, dy = (f >> 1) & 1;
         const int i2 = (a + 1) - dx * N, j2 = (b + 1) - dy * N;
-        vals[cidx] = A.contrib_hi[((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + i2 + N1 * j2];
+        vals[cidx] = __ldcg(A.contrib_hi + ((long)(ex + dx) + (long)A.Ex * (ey + dy)) * (N1 * N1) + i2 + N1 * j2);
       } else {
         vals[cidx] = sh[off];
       }
@@ -428,6 +443,9 @@ __global__ void k_sem_k2(SemArgs A) {
   const int q = threadIdx.x / NSH;
   const int s = threadIdx.x - q * NSH;
   const int ex = blockIdx.x * k2_eb(N) + q, ey = blockIdx.y, ez = blockIdx.z + A.k2_z0;
+  // top-layer blocks (dispatched last: blockIdx.z is the slowest grid index) read the
+  // upper rank's contributions: wait for them here instead of on the stream
+  if (A.k2_wait && ez == A.Ezl - 1) block_wait_flag(A.k2_wait, A.k2_wait_v);
   if (q >= k2_eb(N) || ex >= A.Ex) return;
   const long e = ex + (long)A.Ex * (ey + (long)A.Ey * ez);
   k2_node<N, EPI>(A, e, ex, ey, ez, s);

@@ -17,6 +17,22 @@
 //   4. divergence (r rows, s columns accumulate, t on the column) ->
 //      epilogue: interior nodes finished in place, shell nodes to K2.
 
+// Element of this K1 block.  With an in-kernel halo wait (A.k1_wait) the grid
+// is rotated by one element layer: layers 1.. come first and the layer-0 blocks,
+// the only readers of the lower rank's halo, are dispatched last.
+__device__ __forceinline__ long k1_element(const SemArgs& A) {
+  const long ne = A.e_end - A.e_begin;
+  long bi = blockIdx.x;
+  if (A.k1_wait) {
+    bi += (long)A.Ex * A.Ey;
+    if (bi >= ne) bi -= ne;
+  }
+  return A.e_begin + bi;
+}
+__device__ __forceinline__ void k1_halo_wait(const SemArgs& A, long e) {
+  if (A.k1_wait && e < (long)A.Ex * A.Ey) block_wait_flag(A.k1_wait, A.k1_wait_v);
+}
+
 template <int N, int EPI, int KS>
 struct K1L {
   using S = K3Smem<N, EPI>;
@@ -34,7 +50,7 @@ struct K1L {
     const int ay = owner1d<N>(ey, tb, A.Ey, oey);
     const bool xy_ok = ax >= 0 && ay >= 0;
     const double* ptr[KH];
-    bool ok[KH];
+    bool ok[KH], from_halo[KH];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       int oez = 0;
@@ -44,11 +60,13 @@ struct K1L {
       const long own = ((long)oex + (long)A.Ex * ((long)oey + (long)A.Ey * lz)) * NOS +
                        sem_pos(N, xy_ok ? ax : 0, xy_ok ? ay : 0, az >= 0 ? az : 0);
       const long halo = ((long)oex + (long)A.Ex * oey) * (N * N) + ax + N * ay;
-      ptr[q] = (lz < 0) ? A.halo_lo + halo : A.u + own;
+      from_halo[q] = lz < 0;
+      ptr[q] = from_halo[q] ? A.halo_lo + halo : A.u + own;
     }
     double v[KH];
+    // the halo may be written by a peer during this kernel (in-kernel wait): L2-only load for it
 #pragma unroll
-    for (int q = 0; q < KH; ++q) v[q] = ok[q] ? __ldg(ptr[q]) : 0.0;
+    for (int q = 0; q < KH; ++q) v[q] = ok[q] ? (from_halo[q] ? __ldcg(ptr[q]) : __ldg(ptr[q])) : 0.0;
 #pragma unroll
     for (int q = 0; q < KH; ++q) su[idx(ta, tb, O0 + q)] = v[q];
   }
@@ -201,7 +219,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
   double* ss = sm + S::s_off;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
   const int t = threadIdx.x;
-  const long e = A.e_begin + blockIdx.x;
+  const long e = k1_element(A);
   const int line = t % (N1 * N1);
   const int h = t / (N1 * N1);  // line part: warp-uniform for N1*N1 a multiple of 32
   const int ta = line % N1, tb = line / N1;
@@ -231,6 +249,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
       default: L::template fn<3 % KS>(__VA_ARGS__); break; \
     }                                                      \
   } while (0)
+  k1_halo_wait(A, e);
   ON_PART(gather, A, su, ta, tb, e);
   __syncthreads();
   ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
   double* ss = sm + S::s_off;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
   const int t = threadIdx.x;
-  const long e = A.e_begin + blockIdx.x;
+  const long e = k1_element(A);
   const int line = t % (N1 * N1);
   const int h = t / (N1 * N1);
   const int ta = line % N1, tb = line / N1;
@@ -287,6 +306,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
       asm volatile("prefetch.global.L2 [%0];" ::"l"(Ge + q * 16));
   }
   double wt[KH], dvh[KH];
+  k1_halo_wait(A, e);
   ON_PART(gather, A, su, ta, tb, e);
   __syncthreads();
   ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);

@@ -555,6 +555,19 @@ struct SemLevel final : cmg_op {
     peer.on = total == static_cast<double>(R);
   }
 
+  // In-kernel waits for the peer exchanges (CMG_PEER_KWAIT, default on): the
+  // element work that does not read the neighbour's data runs while it is in
+  // flight, without splitting K1/K2 into extra launches.  K1's rotated grid is
+  // implemented by the line kernels (order >= 5); other orders wait on the stream.
+  static bool kwait() {
+    static const bool on = [] {
+      const char* env = std::getenv("CMG_PEER_KWAIT");
+      return !(env && std::atoi(env) == 0);
+    }();
+    return on;
+  }
+  bool kwait_k1() const { return kwait() && N >= 5 && (N + 1) % 2 == 0; }
+
   void run_peer(int mode, int epi, SemArgs& a) {
     cudaStream_t s = ctx->stream;
     SemArgs b = a;
@@ -567,10 +580,16 @@ struct SemLevel final : cmg_op {
         stream_write(s, peer.flags_up + 0, k);
       }
       if (down() >= 0) {
-        stream_wait(s, peer.flags + 0, k);
         b.halo_lo = peer.hsend_dn + (k & 1) * peer.hn;
+        if (kwait_k1()) {  // only the layer-0 blocks (dispatched last) wait, inside K1
+          b.k1_wait = peer.flags + 0;
+          b.k1_wait_v = k;
+        } else {
+          stream_wait(s, peer.flags + 0, k);
+        }
       }
       sem_k1(b, mode, epi, s);
+      b.k1_wait = nullptr;
       if (down() >= 0) stream_write(s, peer.flags_dn + 1, k);
     } else {
       sem_k1(b, mode, epi, s);
@@ -584,8 +603,13 @@ struct SemLevel final : cmg_op {
       stream_write(s, peer.flags_dn + 2, k);
     }
     if (up() >= 0) {
-      stream_wait(s, peer.flags + 2, k);
       b.contrib_hi = peer.csend_up + (k & 1) * peer.cn;
+      if (kwait()) {  // only the top-layer blocks (dispatched last) wait, inside K2
+        b.k2_wait = peer.flags + 2;
+        b.k2_wait_v = k;
+      } else {
+        stream_wait(s, peer.flags + 2, k);
+      }
     }
     sem_k2(b, epi, s);
     if (up() >= 0) stream_write(s, peer.flags_up + 3, k);

@@ -73,6 +73,15 @@ struct SemArgs {
   long e_begin = 0, e_end = 0;
   int k2_z0 = 0;  // first local layer of a K2 launch (set by the launcher)
   int prefetch_g = 0;  // K1: L2 prefetch of the element's geometric factors at block start
+  // in-kernel waits on a peer's "ready" epoch (multi-GPU face exchanges over peer
+  // memory): K1 runs its blocks layer 1.. first and only the layer-0 blocks, which
+  // read halo_lo, wait for *k1_wait >= k1_wait_v; in K2 only the top-layer blocks,
+  // which read contrib_hi, wait for *k2_wait >= k2_wait_v.  nullptr: no wait (the
+  // launcher's stream already waited).
+  const unsigned* k1_wait = nullptr;
+  unsigned k1_wait_v = 0;
+  const unsigned* k2_wait = nullptr;
+  unsigned k2_wait_v = 0;
 };
 
 // upload the order-N GLL derivative matrix to constant memory (once per order)

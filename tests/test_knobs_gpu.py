@@ -18,6 +18,7 @@ VARIANTS = [
     ("CMG_PEER_HALO", "0", "tests/test_multigpu.py", "bitwise"),
     # the small test meshes sit below the default peer threshold: force the peer path
     ("CMG_PEER_MIN", "0", "tests/test_multigpu.py", "bitwise"),
+    ("CMG_PEER_KWAIT", "0", "tests/test_multigpu.py", "bitwise"),
     ("CMG_SHELL_LEX", "1", "tests/test_sem_gpu.py", "apply_diag_rhs or sweeps_all_families or v_cycle"),
     ("CMG_CGS_FUSE", "0", "tests/test_sem_gpu.py", "pmg_solves"),
     ("CMG_CGS_FUSE", "0", "tests/test_fd_gpu.py", "golden_solves"),
