@@ -323,3 +323,25 @@ def test_coarse_cg_fallback_under_pgmres_and_pcg_rejected(cm, sem, monkeypatch):
     check_x(P.A.to_canonical(x), ref.x)
     with pytest.raises(ValueError, match="not a fixed linear operator"):
         gpu_solve(cm, P, 2, 2, 2, b, driver=0)
+
+
+@pytest.mark.parametrize("geo", [0, 1])
+def test_tall_mesh_apply_and_sweeps_bitwise(cm, sem, geo):
+    """A taller mesh (12 element layers, 3x2 per layer): operator and sweeps
+    bitwise against the restatement on box and Kershaw geometry."""
+    ex, ey, ez = 3, 2, 12
+    P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez, geometry=geo, eps=0.3), (7, 3, 1))
+    o = ob.OraclePmg((7, 3, 1), ex, ey, ez, geo, 0.3)
+    A = P.ops[0]
+    x = ob.random_vector(o.n[0], 17)
+    y = A.new_vector()
+    A.apply(A.from_canonical(x), y)
+    assert same(A.to_canonical(y), o.sem(0).apply(x))
+    b = ob.random_vector(o.n[0], 3)
+    for fam in (0, 2, 3):
+        for order, xz in ((4, True), (8, False)):
+            cfg = cm.ChebyshevConfig(cm.Family(fam), order, o.lambda_tilde[0])
+            xd = A.from_canonical(np.zeros(o.n[0]) if xz else x)
+            cm.chebyshev_smooth(A, P.inv_diag(0), cfg, order, A.from_canonical(b), xd, xz)
+            ref = o.smooth(0, fam, order, b, np.zeros(o.n[0]) if xz else x, xz)
+            assert same(A.to_canonical(xd), ref), (fam, order, xz)
