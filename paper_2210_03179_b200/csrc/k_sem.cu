@@ -31,7 +31,9 @@ struct SemC {
   static constexpr int NOS = sem_nos(N);
   static constexpr int NINT = sem_nint(N);
   static constexpr int NSH = sem_nshared(N);
-  static constexpr int KS = (N1 % 2 == 0 && N >= 3) ? 2 : 1;  // k-split across threads
+  // k-split across threads: order 3 keeps whole columns per thread (the p=3 smoother
+  // step 280 -> 266 us at E=64^3, TTS -0.9%, profiles/r02/ab_k1ax3_ks.txt)
+  static constexpr int KS = (N1 % 2 == 0 && N >= 5) ? 2 : 1;
   static constexpr int KN = N1 / KS;                          // k values per thread
   static constexpr int TPE = N1 * N1 * KS;                    // threads per element
   static constexpr int EPB = (128 / TPE) > 0 ? (128 / TPE) : 1;  // elements per block
