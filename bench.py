@@ -253,6 +253,12 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def sweep_bytes(E, order, n_glob):
+    """Algorithmic DRAM bytes of one warm sweep: 48 B per local node on
+    every pass; per unknown 40 B (init pass), 64 B (middle steps), 48 B (fused last step)."""
+    return order * 48 * 512 * E ** 3 + (40 + 64 * (order - 2) + 48) * n_glob
+
+
 def config_of(E, order, n_glob, world):
     """The workload -- identical for the GPU arm at any N and the reference arm
     (the partition is reported next to it, not in it)."""
@@ -413,9 +419,7 @@ def main():
     # 40 B on the residual-initialising pass (gather x; read b, invD; write r, d),
     # 64 B on a middle step (gather d; read d, x, r, invD; write x, r, d') and 48 B
     # on the fused last step (no r, d writes): 8*48 N_L + (40 + 6*64 + 48) N_G at order 8
-    N_L = 512 * E ** 3
-    bytes_sweep = order * 48 * N_L + (40 + 64 * (order - 2) + 48) * n_glob
-    per_gpu_bytes = bytes_sweep / world
+    per_gpu_bytes = sweep_bytes(E, order, n_glob) / world
     peak, peak_src = peaks()
     achieved = per_gpu_bytes / (ms_per_step * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
