@@ -677,18 +677,19 @@ void pgmres(cmg_op* A, cmg_precond* M, const double* b, const double* x0, double
   // scalars of the Arnoldi cycle: the context's fixed slots up to restart 63,
   // else a workspace sized for m (any restart >= 1, krylov.hpp:148)
   double *coef = dsc + S_COEF, *coef2 = dsc + S_COEF2, *H = dsc + S_H, *Hs = dsc + S_HS, *g = dsc + S_G,
-         *y = dsc + S_Y, *lsq_work = nullptr;
+         *y = dsc + S_Y;
   if (m > 63) {
     const std::size_t nh = static_cast<std::size_t>(m + 1) * m;
-    WBuf sc = wsbuf(c, 8, 2 * (m + 1) + 2 * nh + (m + 1) + m + gmres_lsq_work(m));
+    WBuf sc = wsbuf(c, 8, 2 * (m + 1) + 2 * nh + (m + 1) + m);
     coef = sc.p;
     coef2 = coef + (m + 1);
     H = coef2 + (m + 1);
     Hs = H + nh;
     g = Hs + nh;
     y = g + (m + 1);
-    lsq_work = y + m;
   }
+  // global working copy of the least-squares solve, used when it exceeds shared memory
+  double* lsq_work = wsbuf(c, 9, gmres_lsq_work(m)).p;
   const bool fuse_ok = m <= 63;
   bool done = false;
   while (!done && R.iterations < o.maxit) {

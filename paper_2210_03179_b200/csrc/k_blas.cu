@@ -5,6 +5,7 @@
 // reference's sequential C++ (krylov.hpp:144-264, no -march in its CMake),
 // so the only difference from the reference is the summation ORDER of the
 // inner products (fixed two-stage tree here, left-to-right there).
+#include <cstdlib>
 #include "cmg_internal.hpp"
 
 namespace cmg {
@@ -486,14 +487,19 @@ std::size_t gmres_lsq_work(int m) { return (std::size_t)(m + 1) * m + 2 * (std::
 
 void launch_gmres_lsq(const double* H, int m, int j, double, const double* beta_dev, double* Hs,
                       double* g, double* y, double* gwork, cudaStream_t s) {
-  constexpr std::size_t kMaxSmem = 227 * 1024;
+  static constexpr std::size_t kMaxSmem = 227 * 1024;
   static bool configured = false;
+  // CMG_LSQ_SMEM_MAX (bytes, test knob): below it the working copy lives in shared memory
+  static const std::size_t smem_max = [] {
+    const char* env = std::getenv("CMG_LSQ_SMEM_MAX");
+    return env ? std::min<std::size_t>(kMaxSmem, std::strtoull(env, nullptr, 10)) : kMaxSmem;
+  }();
   if (!configured) {
     CMG_CUDA(cudaFuncSetAttribute(k_gmres_lsq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
     configured = true;
   }
   const std::size_t bytes = gmres_lsq_work(j + 1) * sizeof(double);
-  if (bytes <= kMaxSmem) k_gmres_lsq<<<1, 32, bytes, s>>>(H, m, j, beta_dev, Hs, g, y, nullptr);
+  if (bytes <= smem_max) k_gmres_lsq<<<1, 32, bytes, s>>>(H, m, j, beta_dev, Hs, g, y, nullptr);
   else k_gmres_lsq<<<1, 32, 0, s>>>(H, m, j, beta_dev, Hs, g, y, gwork);
   CMG_LAUNCH_CHECK();
 }

@@ -23,6 +23,8 @@ VARIANTS = [
     ("CMG_CGS_FUSE", "0", "tests/test_sem_gpu.py", "pmg_solves"),
     ("CMG_CGS_FUSE", "0", "tests/test_fd_gpu.py", "golden_solves"),
     ("CMG_FD_GRAPHS", "0", "tests/test_fd_gpu.py", "golden_solves or preconditioner_cost"),
+    # the PGMRES least-squares working copy in global memory (the path for restart > ~169)
+    ("CMG_LSQ_SMEM_MAX", "0", "tests/test_fd_gpu.py", "any_restart"),
     ("CMG_SCHWARZ_MMA", "1", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_SCHWARZ_SMALL", "0", "tests/test_sem_gpu.py", "schwarz"),
     ("CMG_SCHWARZ_IL", "1", "tests/test_sem_gpu.py", "schwarz"),
