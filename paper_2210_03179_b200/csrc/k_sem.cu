@@ -1251,7 +1251,7 @@ constexpr int LCH = 16;
 // leaves the registers to unroll the stride loop so several loads are in
 // flight per thread. Either way each accumulator sums its terms in ascending
 // q and the block reduction is the same, so the partials keep their bits.
-template <int MAXC>
+template <int MAXC, int UNR = (MAXC == 1 ? 4 : 1)>
 __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int nv,
                              const double* __restrict__ w, long layer_len, int nlayers,
                              double* __restrict__ partials) {
@@ -1262,8 +1262,29 @@ __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int 
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
   const long base = (long)layer * layer_len;
+  const long step = (long)LCH * blockDim.x;
+  long q = (long)chunk * blockDim.x + threadIdx.x;
+  if constexpr (MAXC > 1 && UNR > 1) {
+    // UNR strides' loads issued together; each accumulator still adds its terms in
+    // ascending q, so the partials keep their bits
+    for (; q + (UNR - 1) * step < layer_len; q += UNR * step) {
+      double wv[UNR], vv[UNR][MAXC];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        wv[u] = w[base + q + u * step];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c)
+          vv[u][c] = c < cnt ? V[(std::size_t)(v0 + c) * ldv + base + q + u * step] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c)
+          if (c < cnt) acc[c] += vv[u][c] * wv[u];
+    }
+  }
 #pragma unroll(MAXC == 1 ? 4 : 1)
-  for (long q = (long)chunk * blockDim.x + threadIdx.x; q < layer_len; q += (long)LCH * blockDim.x) {
+  for (; q < layer_len; q += step) {
     const double wv = w[base + q];
 #pragma unroll
     for (int c = 0; c < MAXC; ++c)
@@ -1291,7 +1312,7 @@ __global__ void k_layer_dots(const double* __restrict__ V, std::size_t ldv, int 
 // unfused update + layer dots, V is streamed from HBM once.
 // MAXV: compile-time bound on nv (8/16/32) so the accumulators of short bases
 // do not cost the registers of long ones.
-template <int MAXV>
+template <int MAXV, int UNR = 1>
 __global__ void __launch_bounds__(256) k_layer_cgs_dots(const double* __restrict__ V, std::size_t ldv, int nv,
                                                         const double* __restrict__ coef, double* __restrict__ w,
                                                         long layer_len, int nlayers, double* hcol, int hstride,
@@ -1307,7 +1328,33 @@ __global__ void __launch_bounds__(256) k_layer_cgs_dots(const double* __restrict
 #pragma unroll
   for (int q = 0; q < MAXV; ++q) acc[q] = 0.0;
   const long base = (long)layer * layer_len;
-  for (long q = (long)chunk * blockDim.x + threadIdx.x; q < layer_len; q += (long)LCH * blockDim.x) {
+  const long step = (long)LCH * blockDim.x;
+  long q0 = (long)chunk * blockDim.x + threadIdx.x;
+  if constexpr (UNR > 1 && MAXV <= 16) {
+    // UNR strides at once: all their loads in flight together; per entry the same
+    // update chain, per accumulator the same ascending-q order (same bits)
+    for (; q0 + (UNR - 1) * step < layer_len; q0 += UNR * step) {
+      double v[UNR], vv[UNR][MAXV];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const std::size_t i = base + q0 + u * step;
+        v[u] = w[i];
+#pragma unroll
+        for (int l = 0; l < MAXV; ++l) vv[u][l] = l < nv ? V[(std::size_t)l * ldv + i] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+        for (int l = 0; l < MAXV; ++l)
+          if (l < nv) v[u] = __dadd_rn(v[u], __dmul_rn(-c[l], vv[u][l]));
+        w[base + q0 + u * step] = v[u];
+#pragma unroll
+        for (int l = 0; l < MAXV; ++l)
+          if (l < nv) acc[l] += vv[u][l] * v[u];
+      }
+    }
+  }
+  for (long q = q0; q < layer_len; q += step) {
     const std::size_t i = base + q;
     double v = w[i];
     if constexpr (MAXV <= 16) {  // the basis entries stay in registers for both uses
@@ -1521,10 +1568,20 @@ void sem_restrict_local(const SemArgs& f, int Nc, const double* J, const double*
 void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
                     int nlayers, double* partials, double* out, cudaStream_t s) {
   dim3 grid(LCH, nlayers, (nv + 7) / 8);
+  // CMG_DOTS_UNROLL: strides per load batch of the multi-dots (E=64^3 solve, 8 launches:
+  // 1 -> 11.2 ms at 3.4 TB/s, 2 -> 8.6 ms, 4 -> 6.6 ms at 5.8 TB/s; profiles/r02/ab_dots.txt)
+  static const int unr = [] {
+    const char* env = std::getenv("CMG_DOTS_UNROLL");
+    return env ? std::atoi(env) : 4;
+  }();
   if (nv == 1)
     k_layer_dots<1><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+  else if (unr >= 4)
+    k_layer_dots<8, 4><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+  else if (unr == 2)
+    k_layer_dots<8, 2><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
   else
-    k_layer_dots<8><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
+    k_layer_dots<8, 1><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
   CMG_LAUNCH_CHECK();
   const long t = (long)nv * nlayers;
   k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
@@ -1534,7 +1591,19 @@ void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, l
 void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* coef, double* w, long layer_len,
                         int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s) {
   dim3 grid(LCH, nlayers, 1);
-  if (nv <= 8) k_layer_cgs_dots<8><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  // CMG_CGS_UNROLL: strides per load batch of the fused CGS pass (8 launches at E=64^3:
+  // 1 -> 10.3 ms at 3.6 TB/s, 2 -> 7.2 ms at 5.2 TB/s; profiles/r02/ab_dots.txt)
+  static const int unr = [] {
+    const char* env = std::getenv("CMG_CGS_UNROLL");
+    return env ? std::atoi(env) : 2;
+  }();
+  if (nv <= 8 && unr >= 3)
+    k_layer_cgs_dots<8, 3><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  else if (nv <= 8 && unr == 2)
+    k_layer_cgs_dots<8, 2><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  else if (nv <= 8) k_layer_cgs_dots<8><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
+  else if (nv <= 16 && unr >= 2)
+    k_layer_cgs_dots<16, 2><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   else if (nv <= 16) k_layer_cgs_dots<16><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   else k_layer_cgs_dots<32><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   CMG_LAUNCH_CHECK();

@@ -21,6 +21,8 @@ VARIANTS = [
     ("CMG_PEER_KWAIT", "0", "tests/test_multigpu.py", "bitwise"),
     ("CMG_SHELL_LEX", "1", "tests/test_sem_gpu.py", "apply_diag_rhs or sweeps_all_families or v_cycle"),
     ("CMG_CGS_FUSE", "0", "tests/test_sem_gpu.py", "pmg_solves"),
+    ("CMG_DOTS_UNROLL", "1", "tests/test_sem_gpu.py", "pmg_solves or determinism"),
+    ("CMG_CGS_UNROLL", "1", "tests/test_sem_gpu.py", "pmg_solves or determinism"),
     ("CMG_CGS_FUSE", "0", "tests/test_fd_gpu.py", "golden_solves"),
     ("CMG_FD_GRAPHS", "0", "tests/test_fd_gpu.py", "golden_solves or preconditioner_cost"),
     # the PGMRES least-squares working copy in global memory (the path for restart > ~169)
