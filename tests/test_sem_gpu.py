@@ -345,3 +345,46 @@ def test_tall_mesh_apply_and_sweeps_bitwise(cm, sem, geo):
             cm.chebyshev_smooth(A, P.inv_diag(0), cfg, order, A.from_canonical(b), xd, xz)
             ref = o.smooth(0, fam, order, b, np.zeros(o.n[0]) if xz else x, xz)
             assert same(A.to_canonical(xd), ref), (fam, order, xz)
+
+
+@pytest.mark.parametrize("E", [(1, 1, 1), (2, 1, 1), (1, 2, 3)])
+def test_degenerate_meshes_empty_coarse_level(cm, sem, E):
+    """One-element-thick meshes: the p=1 level has no interior unknowns (an empty
+    coarse solve), the p=3 level a handful -- counts and histories as the
+    reference templates (which accept an empty BandedCholesky)."""
+    R, b, ref, _ = ref_solve_with_floor(*E, 0, 1.0, 0, 2, 4, 0, floor=False)
+    assert R.n[2] == 0
+    P = sem.PMGHierarchy(sem.SemDesc(7, *E), (7, 3, 1))
+    x, rep = gpu_solve(cm, P, 2, 4, 0, b)
+    assert (rep.iterations, rep.fine_matvecs, rep.status) == (ref.iterations, ref.fine_matvecs, ref.status)
+    check_history(rep.residual_history, ref.history, 0.0, f"mesh {E}")
+    check_x(P.A.to_canonical(x), ref.x, f"mesh {E}")
+
+
+@pytest.mark.parametrize("case", ["zero_rhs", "maxit", "restart1", "pcg"])
+def test_sem_solver_edge_cases(cm, sem, case):
+    """krylov.hpp edge paths on the SEM operator vs the reference templates: a zero
+    right-hand side ("zero initial residual", x = 0), maxit reached mid-cycle,
+    restart = 1 (every iteration restarts), PCG with a symmetric (2,2) cycle."""
+    ex = ey = ez = 3
+    R = ob.RefPmg((7, 3, 1), ex, ey, ez)
+    b = np.zeros(R.n[0]) if case == "zero_rhs" else R.sem(0).rhs()
+    drv, kpre, kpost, kw = 1, 4, 0, {}
+    if case == "maxit":
+        kw = {"maxit": 3}
+    elif case == "restart1":
+        kw = {"restart": 1}
+    elif case == "pcg":
+        drv, kpre, kpost = 0, 2, 2
+    ref = R.solve(drv, 2, kpre, kpost, b, tol=1e-8, **kw)
+    P = sem.PMGHierarchy(sem.SemDesc(7, ex, ey, ez), (7, 3, 1))
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), kpre, kpost)
+    fn = cm.pgmres if drv == 1 else cm.pcg
+    x, rep = fn(P.A, P.preconditioner(cyc), P.A.from_canonical(b), None, cm.SolveOptions(tol=1e-8, **kw))
+    assert (rep.iterations, rep.fine_matvecs, rep.status, rep.converged) == (
+        ref.iterations, ref.fine_matvecs, ref.status, ref.converged)
+    if case == "zero_rhs":
+        assert rep.residual_history == [0.0] and not np.any(P.A.to_canonical(x))
+        return
+    check_history(rep.residual_history, ref.history, 0.0, case)
+    check_x(P.A.to_canonical(x), ref.x, case)
