@@ -483,8 +483,11 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
     constexpr unsigned nt = (N + 1) * (N + 1) * 2;
     SemArgs b = a;
     b.prefetch_g = pf;
-    if (greg) k_sem_k1_greg<N, EPI, 2, 8><<<(unsigned)ne, nt, K3Smem<N, EPI, false>::bytes, s>>>(b);
-    else k_sem_k1_lines<N, EPI, 2><<<(unsigned)ne, nt, K3Smem<N, EPI>::bytes, s>>>(b);
+    const long LE = (long)a.Ex * a.Ey;  // [e_begin, e_end) is whole element layers
+    b.k1_z0 = (int)(a.e_begin / LE);
+    const dim3 grid((unsigned)a.Ex, (unsigned)a.Ey, (unsigned)(ne / LE));
+    if (greg) k_sem_k1_greg<N, EPI, 2, 8><<<grid, nt, K3Smem<N, EPI, false>::bytes, s>>>(b);
+    else k_sem_k1_lines<N, EPI, 2><<<grid, nt, K3Smem<N, EPI>::bytes, s>>>(b);
   } else if constexpr (MODE == SEM_AX) {
     if constexpr (N == 3) {
       // order 3: the register-factor line kernel, one element (one warp) per
@@ -500,7 +503,11 @@ void launch_k1(const SemArgs& a, cudaStream_t s) {
         return 0;
       }();
       if (g3) {
-        k_sem_k1_greg<3, EPI, 2, 16><<<(unsigned)ne, 32, K3Smem<3, EPI, false>::bytes, s>>>(a);
+        SemArgs b = a;
+        const long LE = (long)a.Ex * a.Ey;
+        b.k1_z0 = (int)(a.e_begin / LE);
+        const dim3 grid((unsigned)a.Ex, (unsigned)a.Ey, (unsigned)(ne / LE));
+        k_sem_k1_greg<3, EPI, 2, 16><<<grid, 32, K3Smem<3, EPI, false>::bytes, s>>>(b);
         CMG_LAUNCH_CHECK();
         return;
       }

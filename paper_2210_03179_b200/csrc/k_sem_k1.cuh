@@ -17,20 +17,28 @@
 //   4. divergence (r rows, s columns accumulate, t on the column) ->
 //      epilogue: interior nodes finished in place, shell nodes to K2.
 
-// Element of this K1 block.  With an in-kernel halo wait (A.k1_wait) the grid
-// is rotated by one element layer: layers 1.. come first and the layer-0 blocks,
-// the only readers of the lower rank's halo, are dispatched last.
-__device__ __forceinline__ long k1_element(const SemArgs& A) {
-  const long ne = A.e_end - A.e_begin;
-  long bi = blockIdx.x;
-  if (A.k1_wait) {
-    bi += (long)A.Ex * A.Ey;
-    if (bi >= ne) bi -= ne;
-  }
-  return A.e_begin + bi;
+// Element of this K1 block.  The grid is (Ex, Ey, layers) from layer A.k1_z0 on,
+// so the coordinates need no division (64-bit divisions by the runtime Ex, Ey
+// were ~10% of K1's instructions).  With an in-kernel halo wait (A.k1_wait) the
+// layers are rotated by one: layers 1.. come first and the layer-0 blocks, the
+// only readers of the lower rank's halo, are dispatched last (z is the slowest
+// grid index).
+struct K1Elem {
+  int ex, ey, ez;  // ez: local layer
+  long e;
+};
+__device__ __forceinline__ K1Elem k1_element(const SemArgs& A) {
+  int zb = blockIdx.z;
+  if (A.k1_wait && ++zb == (int)gridDim.z) zb = 0;
+  K1Elem r;
+  r.ex = blockIdx.x;
+  r.ey = blockIdx.y;
+  r.ez = A.k1_z0 + zb;
+  r.e = r.ex + (long)A.Ex * (r.ey + (long)A.Ey * r.ez);
+  return r;
 }
-__device__ __forceinline__ void k1_halo_wait(const SemArgs& A, long e) {
-  if (A.k1_wait && e < (long)A.Ex * A.Ey) block_wait_flag(A.k1_wait, A.k1_wait_v);
+__device__ __forceinline__ void k1_halo_wait(const SemArgs& A, const K1Elem& el) {
+  if (A.k1_wait && el.ez == 0) block_wait_flag(A.k1_wait, A.k1_wait_v);
 }
 
 template <int N, int EPI, int KS>
@@ -42,9 +50,9 @@ struct K1L {
   __device__ static constexpr int idx(int i, int j, int k) { return ((k * N1 + j) * R + i); }
 
   template <int H>
-  __device__ static void gather(const SemArgs& A, double* su, int ta, int tb, long e) {
+  __device__ static void gather(const SemArgs& A, double* su, int ta, int tb, const K1Elem& el) {
     constexpr int O0 = H * KH;
-    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+    const int ex = el.ex, ey = el.ey, ez = el.ez;
     int oex = 0, oey = 0;
     const int ax = owner1d<N>(ex, ta, A.Ex, oex);
     const int ay = owner1d<N>(ey, tb, A.Ey, oey);
@@ -219,7 +227,8 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
   double* ss = sm + S::s_off;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
   const int t = threadIdx.x;
-  const long e = k1_element(A);
+  const K1Elem el = k1_element(A);
+  const long e = el.e;
   const int line = t % (N1 * N1);
   const int h = t / (N1 * N1);  // line part: warp-uniform for N1*N1 a multiple of 32
   const int ta = line % N1, tb = line / N1;
@@ -249,8 +258,8 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
       default: L::template fn<3 % KS>(__VA_ARGS__); break; \
     }                                                      \
   } while (0)
-  k1_halo_wait(A, e);
-  ON_PART(gather, A, su, ta, tb, e);
+  k1_halo_wait(A, el);
+  ON_PART(gather, A, su, ta, tb, el);
   __syncthreads();
   ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
   __syncthreads();
@@ -281,7 +290,8 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
   double* ss = sm + S::s_off;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + S::bar_off);
   const int t = threadIdx.x;
-  const long e = k1_element(A);
+  const K1Elem el = k1_element(A);
+  const long e = el.e;
   const int line = t % (N1 * N1);
   const int h = t / (N1 * N1);
   const int ta = line % N1, tb = line / N1;
@@ -306,8 +316,8 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
       asm volatile("prefetch.global.L2 [%0];" ::"l"(Ge + q * 16));
   }
   double wt[KH], dvh[KH];
-  k1_halo_wait(A, e);
-  ON_PART(gather, A, su, ta, tb, e);
+  k1_halo_wait(A, el);
+  ON_PART(gather, A, su, ta, tb, el);
   __syncthreads();
   ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
   __syncthreads();

@@ -72,6 +72,7 @@ struct SemArgs {
   // K2 needs whole element layers)
   long e_begin = 0, e_end = 0;
   int k2_z0 = 0;  // first local layer of a K2 launch (set by the launcher)
+  int k1_z0 = 0;  // first local layer of a K1 line-kernel launch (grid = Ex x Ey x layers; set by the launcher)
   int prefetch_g = 0;  // K1: L2 prefetch of the element's geometric factors at block start
   // in-kernel waits on a peer's "ready" epoch (multi-GPU face exchanges over peer
   // memory): K1 runs its blocks layer 1.. first and only the layer-0 blocks, which
