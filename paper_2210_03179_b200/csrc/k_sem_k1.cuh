@@ -47,7 +47,24 @@ struct K1L {
   static constexpr int N1 = N + 1, NP = N1 * N1 * N1, NOS = sem_nos(N), NOPS = S::NOPS, NIP = S::NIP;
   static constexpr int R = N1 + 1, KH = N1 / KS;
   static_assert(N1 % KS == 0, "line split must divide N+1");
-  __device__ static constexpr int idx(int i, int j, int k) { return ((k * N1 + j) * R + i); }
+  // Shared-memory position of node (i,j,k) in the u/r/s line buffers.  A warp's
+  // 32 threads own lines (ta, tb), ta in 0..7 and tb in 4 consecutive values,
+  // and each LDS.64/STS.64 is one wavefront only if the 32 addresses are
+  // distinct mod 32 doubles.  The padded layout (row pitch N+2) is conflict-free
+  // along i and j but 2-way for the thread's own column (i = ta, j = tb), which
+  // the gather, geometry, t-contraction and epilogue touch 28 loads + 16 stores
+  // per element (ncu: 29% / 38% excess shared wavefronts, L1 data pipe 92-95%).
+  // For N+1 = 8 the XOR-swizzled layout 72k + 8j + (i ^ j) is conflict-free in
+  // all three directions (column 8(tb + k) + (ta ^ tb), j-lines 8(tb + m) +
+  // (ta ^ m), i-lines 8(ta + tb) + (m ^ ta)); each row stays a permutation of
+  // its 8 slots.  Measured: L1 pipe 95 -> 81%, K1 1.70 -> 1.64 ms, sweep +3.7%
+  // (profiles/r02/ab_k1_swizzle_grid3.txt; before the division-free grid the
+  // extra XOR address math cost more than it saved, ab_k1_xor_swizzle.log).
+  static constexpr bool SWZ = (N1 == 8);
+  __device__ static constexpr int idx(int i, int j, int k) {
+    if constexpr (SWZ) return k * 72 + j * 8 + (i ^ j);
+    else return ((k * N1 + j) * R + i);
+  }
 
   template <int H>
   __device__ static void gather(const SemArgs& A, double* su, int ta, int tb, const K1Elem& el) {
