@@ -400,6 +400,20 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
   const int n = head & 0xff, a = (head >> 8) & 0xff, b = (head >> 16) & 0xff, c = head >> 24;
   // padding (far domain boundary) is not an unknown
   if (ex * N + a + 1 >= N * A.Ex || ey * N + b + 1 >= N * A.Ey || (A.z0 + ez) * N + c + 1 >= N * A.Ez) return;
+  // the epilogue operands first: their loads are independent of the contributions,
+  // so all of a thread's loads are in flight together (K2 is memory-latency bound)
+  const long slot = e * NOS + NINT + s;
+  double dv = 0.0, o0 = 0.0, o1 = 0.0, o2 = 0.0;
+  if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) {
+    dv = A.d[slot];
+    if (!A.x_zero) o0 = A.x[slot];
+    o1 = epi_op<EPI>(A, 1)[slot];
+    o2 = A.invd[slot];
+  } else {
+    if constexpr (EpiOps<EPI>::n > 0) o0 = epi_op<EPI>(A, 0)[slot];
+    if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
+    if constexpr (EpiOps<EPI>::n > 2) o2 = epi_op<EPI>(A, 2)[slot];
+  }
   const double* sh = A.shell + e * A.nshell;
   const bool top = ez + 1 >= A.Ezl;  // the dz=1 contributions come from the halo
   double vals[8];
@@ -422,18 +436,6 @@ __device__ __forceinline__ void k2_node(const SemArgs& A, long e, int ex, int ey
 #pragma unroll
   for (int cidx = 0; cidx < 8; ++cidx)
     if (cidx < n) sum += vals[cidx];
-  const long slot = e * NOS + NINT + s;
-  double dv = 0.0, o0 = 0.0, o1 = 0.0, o2 = 0.0;
-  if constexpr (EPI == EPI_CHEB4 || EPI == EPI_CHEB1) {
-    dv = A.d[slot];
-    if (!A.x_zero) o0 = A.x[slot];
-    o1 = epi_op<EPI>(A, 1)[slot];
-    o2 = A.invd[slot];
-  } else {
-    if constexpr (EpiOps<EPI>::n > 0) o0 = epi_op<EPI>(A, 0)[slot];
-    if constexpr (EpiOps<EPI>::n > 1) o1 = epi_op<EPI>(A, 1)[slot];
-    if constexpr (EpiOps<EPI>::n > 2) o2 = epi_op<EPI>(A, 2)[slot];
-  }
   epilogue<EPI>(A, slot, sum, dv, o0, o1, o2);
 }
 
