@@ -15,6 +15,16 @@ namespace cmg {
 
 namespace {
 
+// element coordinates of a local element index (< 2^31): two 32-bit divisions
+// instead of the 64-bit ones `long % int` compiles to (a software routine)
+__device__ __forceinline__ void elem_xyz(long e, int Ex, int Ey, int& ex, int& ey, int& ez) {
+  const unsigned u = (unsigned)e, q = u / (unsigned)Ex;
+  ex = (int)(u - q * (unsigned)Ex);
+  ez = (int)(q / (unsigned)Ey);
+  ey = (int)(q - (unsigned)ez * (unsigned)Ey);
+}
+
+
 template <int N>
 __device__ __forceinline__ int owner1d_s(int g, int ne, int& oe) {
   if (g <= 0 || g >= N * ne) return -1;
@@ -54,7 +64,9 @@ __global__ void __launch_bounds__(64) k_schwarz_local(SchwarzArgs A) {
   __shared__ __align__(16) double S[3][PB2];
   __shared__ double lam[3][PB];
   const long e = blockIdx.x;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+  int ex, ey, ez;
+  elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
+  ez += A.z0;
   for (int d = 0; d < 3; ++d) {
     const int id = A.sidx[e * 3 + d];
     for (int q = threadIdx.x; q < PB2; q += blockDim.x) S[d][q] = A.S[(long)id * PB2 + q];
@@ -214,7 +226,9 @@ __global__ void __launch_bounds__(64) k_schwarz_local_il(SchwarzArgs A) {
   __shared__ __align__(16) double ST[3][PB2];  // ST[d][m*PB + o] = S[d][o*PB + m]: backward
   __shared__ double lam[3][PB];
   const long e = blockIdx.x;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+  int ex, ey, ez;
+  elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
+  ez += A.z0;
   for (int d = 0; d < 3; ++d) {
     const int id = A.sidx[e * 3 + d];
     for (int q = threadIdx.x; q < PB2; q += blockDim.x) {
@@ -307,7 +321,9 @@ __global__ void __launch_bounds__(EPB * (N + 3) * (N + 3)) k_schwarz_local_small
   const long e = blockIdx.x * (long)EPB + le;
   const bool on = e < E;
   if (on) {
-    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+    int ex, ey, ez;
+  elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
+  ez += A.z0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int id = A.sidx[e * 3 + d];
@@ -419,7 +435,9 @@ __global__ void __launch_bounds__(128) k_schwarz_local_mma(SchwarzArgs A) {
   __shared__ double S[3][PB2];
   __shared__ double lam[3][PB];
   const long e = blockIdx.x;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+  int ex, ey, ez;
+  elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
+  ez += A.z0;
   for (int d = 0; d < 3; ++d) {
     const int id = A.sidx[e * 3 + d];
     for (int q = threadIdx.x; q < PB2; q += blockDim.x) S[d][q] = A.S[(long)id * PB2 + q];
@@ -526,7 +544,9 @@ __global__ void k_asm_gather(SchwarzArgs A, double* __restrict__ y, AsmUpdate u)
       asm_emit(u, y, q, 0.0);
       continue;
     }
-    const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = A.z0 + (int)(e / ((long)A.Ex * A.Ey));
+    int ex, ey, ez;
+  elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
+  ez += A.z0;
     const int gx = ex * N + a + 1, gy = ey * N + b + 1, gz = ez * N + c + 1;
     if (gx >= N * A.Ex || gy >= N * A.Ey || gz >= N * A.Ez) {
       asm_emit(u, y, q, 0.0);

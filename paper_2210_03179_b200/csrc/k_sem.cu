@@ -24,6 +24,16 @@ void host_interp_matrix(int Nf, int Nc, double* J);  // host_setup.cpp
 
 namespace {
 
+// element coordinates of a local element index (< 2^31): two 32-bit divisions
+// instead of the 64-bit ones `long % int` compiles to (a software routine)
+__device__ __forceinline__ void elem_xyz(long e, int Ex, int Ey, int& ex, int& ey, int& ez) {
+  const unsigned u = (unsigned)e, q = u / (unsigned)Ex;
+  ex = (int)(u - q * (unsigned)Ex);
+  ez = (int)(q / (unsigned)Ey);
+  ey = (int)(q - (unsigned)ez * (unsigned)Ey);
+}
+
+
 template <int N>
 struct SemC {
   static constexpr int N1 = N + 1;
@@ -248,9 +258,8 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
     }
   }
   for (int q = threadIdx.x; q < N1 * N1; q += blockDim.x) sD[q / N1][q % N1] = A.D[q];
-  const int ex = active ? (int)(e % A.Ex) : 0;
-  const int ey = active ? (int)((e / A.Ex) % A.Ey) : 0;
-  const int ez = active ? (int)(e / ((long)A.Ex * A.Ey)) : 0;
+  int ex = 0, ey = 0, ez = 0;
+  if (active) elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
   // 2. gather Q u (owner slots / halo / Dirichlet zero) into shared memory
   double* ue = su + (std::size_t)le * NP;
   {
@@ -758,7 +767,8 @@ __device__ __forceinline__ bool slot_valid(const SemArgs& A, long q) {
   const long e = q / NOS;
   int a, b, c;
   if (!sem_abc(N, (int)(q - e * NOS), a, b, c)) return false;
-  const int ex = (int)(e % A.Ex), ey = (int)((e / A.Ex) % A.Ey), ez = (int)(e / ((long)A.Ex * A.Ey));
+  int ex, ey, ez;
+  elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
   return ex * N + a + 1 < N * A.Ex && ey * N + b + 1 < N * A.Ey && (A.z0 + ez) * N + c + 1 < N * A.Ez;
 }
 
@@ -812,9 +822,7 @@ __global__ void __launch_bounds__(128) k_prolong(SemArgs F, SemArgs Cc, const do
   for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
   if (threadIdx.x < TEPB) {
     const long e = e0 + threadIdx.x;
-    sxyz[threadIdx.x][0] = (int)(e % F.Ex);
-    sxyz[threadIdx.x][1] = (int)((e / F.Ex) % F.Ey);
-    sxyz[threadIdx.x][2] = (int)(e / ((long)F.Ex * F.Ey));
+    elem_xyz(e, F.Ex, F.Ey, sxyz[threadIdx.x][0], sxyz[threadIdx.x][1], sxyz[threadIdx.x][2]);
   }
   __syncthreads();
   for (int qq = threadIdx.x; qq < TEPB * UC; qq += blockDim.x) {
@@ -980,7 +988,8 @@ __global__ void __launch_bounds__(32 * kTW) k_prolong_w(SemArgs F, SemArgs Cc, c
   double* t2 = t1 + 32 * P;
   double* uc = t2;
   double* ye = yf + e * NOSF;
-  const int ex = (int)(e % F.Ex), ey = (int)((e / F.Ex) % F.Ey), ez = (int)(e / ((long)F.Ex * F.Ey));
+  int ex, ey, ez;
+  elem_xyz(e, F.Ex, F.Ey, ex, ey, ez);
   // this lane's fine outputs: lines (i, j) = (L & 7, L >> 3), L = lane, lane + 32, nodes k = 1..7;
   // their old values are loaded first (add) so the loads overlap the gather and contractions
   double old[2][F1 - 1];
@@ -1105,7 +1114,8 @@ __global__ void __launch_bounds__(128) k_prolong_tma(SemArgs F, SemArgs Cc, cons
   if (!add)
     for (int q = threadIdx.x; q < NOSF; q += blockDim.x) sy[q] = 0.0;
   for (int q = threadIdx.x; q < F1 * C1; q += blockDim.x) sJ[q] = J[q];
-  const int ex = (int)(e % F.Ex), ey = (int)((e / F.Ex) % F.Ey), ez = (int)(e / ((long)F.Ex * F.Ey));
+  int ex, ey, ez;
+  elem_xyz(e, F.Ex, F.Ey, ex, ey, ez);
   for (int q = threadIdx.x; q < UC; q += blockDim.x) {
     const int a = q % C1, b = (q / C1) % C1, c = q / (C1 * C1);
     int oex = 0, oey = 0, oez = 0;
