@@ -219,6 +219,10 @@ struct K1Smem {
   static constexpr std::size_t bytes = (bar_off + 1) * sizeof(double);
 };
 
+// GLL derivative matrices per order in constant memory: with compile-time
+// indices every D entry becomes a DFMA constant-bank operand (no LDS).
+__constant__ double c_D[8][64];
+
 template <int N, int EPI>
 __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
   using C = SemC<N>;
@@ -262,6 +266,7 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
   if (active) elem_xyz(e, A.Ex, A.Ey, ex, ey, ez);
   // 2. gather Q u (owner slots / halo / Dirichlet zero) into shared memory
   double* ue = su + (std::size_t)le * NP;
+  double ucol[KN];  // this thread's own column (all of it when KS == 1)
   {
     int oex = 0, oey = 0;
     const int ax = owner1d<N>(ex, i, A.Ex, oex);
@@ -282,12 +287,69 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
         }
       }
       ue[(k * N1 + j) * N1 + i] = v;
+      ucol[kk] = v;
     }
   }
   __syncthreads();
   mbar_wait(bar, 0);
   // 3. gradient + geometric factors: w_r, w_s, w_t overwrite G_rr, G_rs, G_rt in place
   double* Ge = sG + (std::size_t)le * 6 * NP;
+  if constexpr (C::KS == 1) {
+    // Whole columns per thread: the k-direction contractions use the thread's own
+    // column from registers and D from constant memory (compile-time k, m), the
+    // i/j rows of D sit in registers; w_t never leaves registers.  Same chains,
+    // same operands as the generic path below (same bits), half the shared traffic.
+    double Di[N1], Dj[N1], DiT[N1], DjT[N1], wtc[KN];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      Di[m] = sD[i][m];
+      Dj[m] = sD[j][m];
+      DiT[m] = sD[m][i];
+      DjT[m] = sD[m][j];
+    }
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      const int l = (k * N1 + j) * N1 + i;
+      double ur = 0.0, us = 0.0, ut = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        ur = __fma_rn(Di[m], ue[(k * N1 + j) * N1 + m], ur);
+        us = __fma_rn(Dj[m], ue[(k * N1 + m) * N1 + i], us);
+        ut = __fma_rn(c_D[N][k * N1 + m], ucol[m], ut);
+      }
+      const double g0 = Ge[l], g1 = Ge[NP + l], g2 = Ge[2 * NP + l];
+      const double g3 = Ge[3 * NP + l], g4 = Ge[4 * NP + l], g5 = Ge[5 * NP + l];
+      Ge[l] = geo3(g0, g1, g2, ur, us, ut);
+      Ge[NP + l] = geo3(g1, g3, g4, ur, us, ut);
+      wtc[k] = geo3(g2, g4, g5, ur, us, ut);
+    }
+    __syncthreads();
+    if (!active) return;
+    const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
+    const double* soe = so + (std::size_t)le * NOPS * NIP;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      double vr = 0.0, vs = 0.0, vt = 0.0;
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        vr = __fma_rn(DiT[m], Ge[(k * N1 + j) * N1 + m], vr);
+        vs = __fma_rn(DjT[m], Ge[NP + (k * N1 + m) * N1 + i], vs);
+        vt = __fma_rn(c_D[N][m * N1 + k], wtc[m], vt);
+      }
+      const double v = vt + (vr + vs);
+      if (ij_interior && k >= 1 && k < N) {
+        const int p = (i - 1) + (N - 1) * ((j - 1) + (N - 1) * (k - 1));
+        double o0 = 0.0, o1 = 0.0, o2 = 0.0;
+        if constexpr (NOPS > 0) o0 = soe[p];
+        if constexpr (NOPS > 1) o1 = soe[NIP + p];
+        if constexpr (NOPS > 2) o2 = soe[2 * NIP + p];
+        epilogue<EPI>(A, e * NOS + p, v, ucol[k], o0, o1, o2);
+      } else {
+        A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int kk = 0; kk < KN; ++kk) {
     const int k = kb + kk;
@@ -336,9 +398,6 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
 }
 
 // ---------------------------------------------------------------- K1 (AX mode, line contractions)
-// GLL derivative matrices per order in constant memory: with compile-time
-// indices every D entry becomes a DFMA constant-bank operand (no LDS).
-__constant__ double c_D[8][64];
 
 // Line-blocked layout: one block = one element, (N+1)^2 threads.  Each
 // contraction is done by a thread owning a whole line of N+1 nodes along the
