@@ -67,7 +67,7 @@ struct K1L {
   }
 
   template <int H>
-  __device__ static void gather(const SemArgs& A, double* su, int ta, int tb, const K1Elem& el) {
+  __device__ static void gather(const SemArgs& A, double* su, int ta, int tb, const K1Elem& el, double* own) {
     constexpr int O0 = H * KH;
     const int ex = el.ex, ey = el.ey, ez = el.ez;
     int oex = 0, oey = 0;
@@ -93,12 +93,15 @@ struct K1L {
 #pragma unroll
     for (int q = 0; q < KH; ++q) v[q] = ok[q] ? (from_halo[q] ? __ldcg(ptr[q]) : __ldg(ptr[q])) : 0.0;
 #pragma unroll
-    for (int q = 0; q < KH; ++q) su[idx(ta, tb, O0 + q)] = v[q];
+    for (int q = 0; q < KH; ++q) {
+      su[idx(ta, tb, O0 + q)] = v[q];
+      own[q] = v[q];
+    }
   }
 
   template <int H>
   __device__ static void gradient(const double* su, double* sr, double* ss, int ta, int tb, double* wt,
-                                  double* dvh) {
+                                  const double* own) {
     constexpr int O0 = H * KH;
     double l[N1];
 #pragma unroll
@@ -119,15 +122,15 @@ struct K1L {
       for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][(O0 + q) * N1 + m], l[m], v);
       ss[idx(ta, O0 + q, tb)] = v;
     }
+    // the thread's own column: its KH gathered values are still in registers
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = su[idx(ta, tb, m)];
+    for (int m = 0; m < N1; ++m) l[m] = (m >= O0 && m < O0 + KH) ? own[m - O0] : su[idx(ta, tb, m)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       double v = 0.0;
 #pragma unroll
       for (int m = 0; m < N1; ++m) v = __fma_rn(c_D[N][(O0 + q) * N1 + m], l[m], v);
       wt[q] = v;
-      dvh[q] = l[O0 + q];
     }
   }
 
@@ -204,12 +207,13 @@ struct K1L {
 
   template <int H>
   __device__ static void finish(const SemArgs& A, const double* su, const double* sr, const double* so, int i,
-                                int j, long e, const double* dvh) {
+                                int j, long e, const double* dvh, const double* wt) {
     constexpr int O0 = H * KH;
     const bool ij_interior = (i >= 1 && i < N && j >= 1 && j < N);
     double l[N1];
+    // w_t of the column: the thread published its own KH values, the rest come from its partner
 #pragma unroll
-    for (int m = 0; m < N1; ++m) l[m] = sr[idx(i, j, m)];
+    for (int m = 0; m < N1; ++m) l[m] = (m >= O0 && m < O0 + KH) ? wt[m - O0] : sr[idx(i, j, m)];
 #pragma unroll
     for (int q = 0; q < KH; ++q) {
       const int k = O0 + q;
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
     }                                                      \
   } while (0)
   k1_halo_wait(A, el);
-  ON_PART(gather, A, su, ta, tb, el);
+  ON_PART(gather, A, su, ta, tb, el, dvh);
   __syncthreads();
   ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
   __syncthreads();
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS) k_sem_k1_lines(SemArgs
   __syncthreads();
   ON_PART(div_s, ss, su, sr, ta, tb, wt);
   __syncthreads();
-  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
+  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh, wt);
 }
 
 // Variant without the 24.6 KB shared-memory stage for the geometric factors:
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
   }
   double wt[KH], dvh[KH];
   k1_halo_wait(A, el);
-  ON_PART(gather, A, su, ta, tb, el);
+  ON_PART(gather, A, su, ta, tb, el, dvh);
   __syncthreads();
   ON_PART(gradient, su, sr, ss, ta, tb, wt, dvh);
   __syncthreads();
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__((N + 1) * (N + 1) * KS, MINB) k_sem_k1_greg(Se
   ON_PART(div_s, ss, su, sr, ta, tb, wt);
   __syncthreads();
   if constexpr (HAS_OPS) mbar_wait(bar, 0);
-  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh);
+  ON_PART(finish, A, su, sr, so, ta, tb, e, dvh, wt);
 }
 
 #undef ON_PART
