@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
         A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
       }
     }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int kk = 0; kk < KN; ++kk) {
     const int k = kb + kk;
@@ -394,6 +393,7 @@ __global__ void __launch_bounds__(SemC<N>::NT) k_sem_k1_ax(SemArgs A) {
     } else {
       A.shell[e * A.nshell + A.lut[(k * N1 + j) * N1 + i]] = v;
     }
+  }
   }
 }
 
