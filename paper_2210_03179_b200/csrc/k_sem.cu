@@ -1324,7 +1324,7 @@ __global__ void __launch_bounds__(128) k_restrict_local(SemArgs F, const double*
 
 // ---------------------------------------------------------------- layer dots
 // partials[(v*L + layer)*LCH + chunk]
-constexpr int LCH = 16;
+constexpr int LCH = 32;
 // MAXC: 8 in general, 1 for the single dots (norms, <v, w>): one accumulator
 // leaves the registers to unroll the stride loop so several loads are in
 // flight per thread. Either way each accumulator sums its terms in ascending

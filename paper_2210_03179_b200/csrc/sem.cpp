@@ -406,7 +406,7 @@ struct SemLevel final : cmg_op {
     mask.alloc(len);
     sem_slot_mask(args(), mask.p, s);
     // per-layer reduction buffers (up to 64 vectors)
-    lpart.alloc(static_cast<std::size_t>(64) * Ezl * 16);
+    lpart.alloc(static_cast<std::size_t>(64) * Ezl * 32);
     lout.alloc(static_cast<std::size_t>(64) * Ezl);
     lgath.alloc(static_cast<std::size_t>(64) * Ez);
     lpr_h.assign(d.nranks, 0);
