@@ -69,7 +69,7 @@ def check_x(x, xr, what="", floor=0.0):
 
 
 @pytest.mark.parametrize("N,ex,ey,ez,geo", [(7, 3, 2, 4, 0), (7, 2, 3, 2, 1), (3, 4, 3, 2, 0), (1, 5, 4, 3, 0),
-                                            (5, 2, 2, 3, 1), (2, 3, 3, 3, 0)])
+                                            (5, 2, 2, 3, 1), (2, 3, 3, 3, 0), (4, 3, 2, 3, 1), (3, 2, 3, 4, 1)])
 def test_apply_diag_rhs(sem, N, ex, ey, ez, geo):
     d = sem.SemDesc(N, ex, ey, ez, geometry=geo, eps=0.3)
     A = sem.SemOperator(d)
@@ -92,18 +92,19 @@ def test_sweeps_all_families(cm, sem):
     o = ob.OraclePmg((7, 3, 1), 3, 2, 2, 1, 0.3)
     for l in (0, 1):
         assert abs(P.lambda_tilde[l] - o.lambda_tilde[l]) <= 1e-11 * o.lambda_tilde[l]
-    A = P.ops[0]
-    b = ob.random_vector(o.n[0], 3)
-    x0 = ob.random_vector(o.n[0], 4)
-    for fam in (0, 1, 2, 3):
-        for order, xz in ((1, True), (4, True), (5, False), (8, False)):
-            cfg = cm.ChebyshevConfig(cm.Family(fam), order, o.lambda_tilde[0])
-            x = A.from_canonical(np.zeros(o.n[0]) if xz else x0)
-            A.reset_applications()
-            cm.chebyshev_smooth(A, P.inv_diag(0), cfg, order, A.from_canonical(b), x, xz)
-            assert A.applications() == (order - 1 if xz else order)
-            ref = o.smooth(0, fam, order, b, np.zeros(o.n[0]) if xz else x0, xz)
-            assert same(A.to_canonical(x), ref), (fam, order, xz)
+    for lev in (0, 1):  # p=7 (line kernels) and p=3 (packed low-order kernel)
+        A = P.ops[lev]
+        b = ob.random_vector(o.n[lev], 3)
+        x0 = ob.random_vector(o.n[lev], 4)
+        for fam in (0, 1, 2, 3):
+            for order, xz in ((1, True), (4, True), (5, False), (8, False)):
+                cfg = cm.ChebyshevConfig(cm.Family(fam), order, o.lambda_tilde[lev])
+                x = A.from_canonical(np.zeros(o.n[lev]) if xz else x0)
+                A.reset_applications()
+                cm.chebyshev_smooth(A, P.inv_diag(lev), cfg, order, A.from_canonical(b), x, xz)
+                assert A.applications() == (order - 1 if xz else order)
+                ref = o.smooth(lev, fam, order, b, np.zeros(o.n[lev]) if xz else x0, xz)
+                assert same(A.to_canonical(x), ref), (lev, fam, order, xz)
 
 
 def test_transfers_and_coarse_solve(sem):
