@@ -16,6 +16,10 @@
 //   3. gradient (r rows, s columns, t on the thread's column) -> G_e grad u;
 //   4. divergence (r rows, s columns accumulate, t on the column) ->
 //      epilogue: interior nodes finished in place, shell nodes to K2.
+// The thread's own half of its column stays in registers between the phases
+// (the gathered u values for the t-gradient and the epilogue, its w_t values
+// for the t-divergence); only the partner's half goes through shared memory.
+// (k_sem_k1_greg, the default, reads the factors into registers instead of 1.)
 
 // Element of this K1 block.  The grid is (Ex, Ey, layers) from layer A.k1_z0 on,
 // so the coordinates need no division (64-bit divisions by the runtime Ex, Ey
