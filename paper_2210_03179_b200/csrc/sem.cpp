@@ -1343,16 +1343,119 @@ void pmg_vcycle(cmg_pmg* p, int l, const cmg_cycle_config& cc, const double* b, 
   if (cc.k_post > 0) pmg_smooth(p, l, cfg, cc.k_post, b, x, false);
 }
 
+// preconditioner_apply for the p-MG hierarchy (multigrid.hpp:94-98).  One V-cycle
+// is ~55 launches; on one GPU each (v, z) pair it is applied to (PGMRES walks
+// V_j -> Z_j, the same buffers in every solve) is captured once into a CUDA
+// graph and replayed as one launch, the captured operator applications and
+// kernel launches re-added to the counters.  Not captured: partitioned
+// hierarchies (their peer-memory handshakes carry per-call epochs), the
+// tolerance-stopped CG coarse solve and the cuSOLVER triangular solves.  The
+// first apply runs directly (lazy workspaces and kernel attributes), a failed
+// capture falls back to direct launches.  CMG_SEM_GRAPHS=0 disables.
 struct PmgPrecond final : cmg_precond {
   cmg_pmg* p = nullptr;
   cmg_cycle_config cfg{};
+  struct Captured {
+    const double* v;
+    double* z;
+    cudaGraphExec_t exec;
+    std::vector<std::size_t> counts;  // operator applications per level
+    unsigned long long launches;
+  };
+  std::vector<Captured> graphs;
+  std::vector<const double*> ws_seen;  // context workspace slots when the graphs were captured
+  cudaStream_t cap = nullptr;
+  bool warm = false, broken = false;
+
+  std::vector<const double*> ws_now() const {
+    std::vector<const double*> v;
+    for (const auto& w : p->ctx->ws) v.push_back(w ? w->p : nullptr);
+    return v;
+  }
+
+  ~PmgPrecond() override {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    if (cap) cudaStreamDestroy(cap);
+  }
   // deformed mesh above CMG_COARSE_DENSE_MAX: the coarse solve is the
   // tolerance-stopped CG (pmg_coarse_solve), so each V-cycle is a slightly
   // different operator
   bool variable() const override { return p->lev.back()->desc.geometry != 0 && p->cn == 0; }
-  void apply(const double* v, double* z) override {
-    CMG_CUDA(cudaMemsetAsync(z, 0, p->lev[0]->len * sizeof(double), ctx->stream));
+
+  bool graph_ok() const {
+    static const bool on = [] {
+      const char* env = std::getenv("CMG_SEM_GRAPHS");
+      return !(env && std::atoi(env) == 0);
+    }();
+    if (!on || broken || graphs.size() >= 128) return false;
+    for (const auto& l : p->lev)
+      if (l->distributed()) return false;
+    const SemLevel* c = p->lev.back().get();
+    return c->desc.geometry == 0 || (p->cn > 0 && p->cinv);
+  }
+  void direct(const double* v, double* z) {
+    CMG_CUDA(cudaMemsetAsync(z, 0, p->lev[0]->len * sizeof(double), p->ctx->stream));
     pmg_vcycle(p, 0, cfg, v, z, true);
+  }
+  void apply(const double* v, double* z) override {
+    if (!warm || !graph_ok()) {
+      direct(v, z);
+      warm = true;
+      return;
+    }
+    if (ws_now() != ws_seen) {  // a context workspace (Schwarz scratch) was reallocated: recapture
+      for (auto& c : graphs) cudaGraphExecDestroy(c.exec);
+      graphs.clear();
+      ws_seen = ws_now();
+    }
+    const Captured* g = nullptr;
+    for (const auto& c : graphs)
+      if (c.v == v && c.z == z) g = &c;
+    if (!g) g = capture(v, z);
+    if (!g) {
+      direct(v, z);
+      return;
+    }
+    CMG_CUDA(cudaGraphLaunch(g->exec, p->ctx->stream));
+    for (std::size_t l = 0; l < p->lev.size(); ++l) p->lev[l]->count += g->counts[l];
+    g_kernel_launches += g->launches;
+  }
+  const Captured* capture(const double* v, double* z) {
+    if (!cap) CMG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CMG_CUDA(cudaStreamSynchronize(p->ctx->stream));
+    std::vector<std::size_t> c0;
+    for (const auto& l : p->lev) c0.push_back(l->count);
+    const unsigned long long l0 = g_kernel_launches.load();
+    cudaStream_t user = p->ctx->stream;
+    p->ctx->stream = cap;
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        direct(v, z);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(cap, &graph) == cudaSuccess) && ok && graph;
+    }
+    p->ctx->stream = user;
+    cudaGraphExec_t exec = nullptr;
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    Captured c{v, z, exec, {}, g_kernel_launches.load() - l0};
+    for (std::size_t l = 0; l < p->lev.size(); ++l) {
+      c.counts.push_back(p->lev[l]->count - c0[l]);
+      p->lev[l]->count = c0[l];  // captured, not executed
+    }
+    g_kernel_launches -= c.launches;
+    if (!ok) {
+      cudaGetLastError();
+      broken = true;
+      return nullptr;
+    }
+    graphs.push_back(std::move(c));
+    ws_seen = ws_now();
+    return &graphs.back();
   }
 };
 

@@ -25,6 +25,7 @@ VARIANTS = [
     ("CMG_CGS_UNROLL", "1", "tests/test_sem_gpu.py", "pmg_solves or determinism"),
     ("CMG_CGS_FUSE", "0", "tests/test_fd_gpu.py", "golden_solves"),
     ("CMG_FD_GRAPHS", "0", "tests/test_fd_gpu.py", "golden_solves or preconditioner_cost"),
+    ("CMG_SEM_GRAPHS", "0", "tests/test_sem_gpu.py", "pmg_solves or schwarz_pmg or kershaw or graph_replayed"),
     # the PGMRES least-squares working copy in global memory (the path for restart > ~169)
     ("CMG_LSQ_SMEM_MAX", "0", "tests/test_fd_gpu.py", "any_restart"),
     ("CMG_SCHWARZ_MMA", "1", "tests/test_sem_gpu.py", "schwarz"),

@@ -248,6 +248,27 @@ def test_determinism(cm, sem):
     assert r1.residual_history == r2.residual_history
 
 
+@pytest.mark.parametrize("smoother,geo", [(0, 0), (2, 0), (1, 0), (0, 1)])
+def test_graph_replayed_preconditioner_same_bits_and_counts(cm, sem, smoother, geo):
+    """On one GPU the p-MG preconditioner captures each (v, z) pair into a CUDA
+    graph after its first apply and replays it (sem.cpp PmgPrecond): the replayed
+    solves must give the bits, histories and operator counts of the direct first
+    solve (the first apply of each solve and of the object runs directly)."""
+    d = sem.SemDesc(7, 4, 3, 3, geometry=geo, eps=0.3)
+    P = sem.PMGHierarchy(d, (7, 3, 1), smoother=smoother)
+    b = P.A.rhs()
+    cyc = cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 2, 1)
+    M = P.preconditioner(cyc)
+    runs = []
+    for _ in range(3):
+        P.A.reset_applications()
+        x, rep = cm.pgmres(P.A, M, b, None, cm.SolveOptions(tol=1e-10, restart=5, maxit=200))
+        runs.append((x.cpu().numpy().tobytes(), rep.residual_history, rep.iterations, rep.fine_matvecs,
+                     P.A.applications()))
+    assert runs[0][2] > 5  # restarts: the same (v, z) pairs are replayed within a solve too
+    assert runs[1] == runs[0] and runs[2] == runs[0]
+
+
 def test_graft_smoke():
     import os
     import sys
