@@ -269,6 +269,29 @@ def test_graph_replayed_preconditioner_same_bits_and_counts(cm, sem, smoother, g
     assert runs[1] == runs[0] and runs[2] == runs[0]
 
 
+def test_graph_recaptured_after_workspace_growth(cm, sem):
+    """The RAS smoother's scratch is a context workspace slot; a larger hierarchy on
+    the same context reallocates it, so the captured V-cycle graphs of the smaller
+    one must be recaptured (PmgPrecond::ws_now), not replayed on freed memory."""
+    def solver(E):
+        P = sem.PMGHierarchy(sem.SemDesc(7, *E), (7, 3, 1), smoother=2)
+        M = P.preconditioner(cm.CycleConfig(cm.ChebyshevConfig(cm.Family.fourth, 1, P.lambda_tilde[0]), 1, 1))
+        b = P.A.rhs()
+
+        def run():
+            x, rep = cm.pgmres(P.A, M, b, None, cm.SolveOptions(tol=1e-10, restart=4, maxit=100))
+            return x.cpu().numpy().tobytes(), rep.residual_history
+        return P, M, run
+
+    P1, M1, run1 = solver((3, 3, 2))
+    first = run1()
+    assert run1() == first
+    P2, M2, run2 = solver((5, 4, 4))
+    run2()
+    assert run1() == first
+    assert run1() == first
+
+
 def test_graft_smoke():
     import os
     import sys
