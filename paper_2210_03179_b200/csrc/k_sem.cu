@@ -1482,6 +1482,27 @@ __global__ void k_layer_reduce(const double* __restrict__ partials, int nv, int 
   out[t] = s;  // out[v*nlayers + layer]
 }
 
+// One GPU: k_layer_reduce and k_layer_finalize in one launch, block per vector --
+// each layer's chunk sum in k_layer_reduce's order, then the layers in
+// k_layer_finalize's ascending order, so the result has the same bits.
+__global__ void k_layer_reduce_final(const double* __restrict__ partials, int nlayers, double* __restrict__ out,
+                                     int do_sqrt) {
+  extern __shared__ double lsum[];
+  const int v = blockIdx.x;
+  for (int l = threadIdx.x; l < nlayers; l += blockDim.x) {
+    const double* p = partials + ((long)v * nlayers + l) * LCH;
+    double s = 0.0;
+    for (int c = 0; c < LCH; ++c) s += p[c];
+    lsum[l] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int l = 0; l < nlayers; ++l) s += lsum[l];
+    out[v] = do_sqrt ? sqrt(s) : s;
+  }
+}
+
 __global__ void k_layer_finalize(const double* __restrict__ g, int nv, const int* __restrict__ lpr,
                                  int nranks, double* __restrict__ out, int do_sqrt) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1643,8 +1664,20 @@ void sem_restrict_local(const SemArgs& f, int Nc, const double* J, const double*
   throw Error(EINVAL_, "unsupported p-multigrid order pair");
 }
 
+static void layer_reduce_launch(const double* partials, int nv, int nlayers, double* out, double* final_out,
+                                int do_sqrt, cudaStream_t s) {
+  if (final_out) {
+    k_layer_reduce_final<<<(unsigned)nv, 128, (std::size_t)nlayers * sizeof(double), s>>>(partials, nlayers,
+                                                                                         final_out, do_sqrt);
+  } else {
+    const long t = (long)nv * nlayers;
+    k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
+  }
+  CMG_LAUNCH_CHECK();
+}
+
 void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
-                    int nlayers, double* partials, double* out, cudaStream_t s) {
+                    int nlayers, double* partials, double* out, cudaStream_t s, double* final_out, int do_sqrt) {
   dim3 grid(LCH, nlayers, (nv + 7) / 8);
   // CMG_DOTS_UNROLL: strides per load batch of the multi-dots (E=64^3 solve, 8 launches:
   // 1 -> 11.2 ms at 3.4 TB/s, 2 -> 8.6 ms, 4 -> 6.6 ms at 5.8 TB/s; profiles/r02/ab_dots.txt)
@@ -1661,13 +1694,12 @@ void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, l
   else
     k_layer_dots<8, 1><<<grid, 256, 0, s>>>(V, ldv, nv, w, layer_len, nlayers, partials);
   CMG_LAUNCH_CHECK();
-  const long t = (long)nv * nlayers;
-  k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
-  CMG_LAUNCH_CHECK();
+  layer_reduce_launch(partials, nv, nlayers, out, final_out, do_sqrt, s);
 }
 
 void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* coef, double* w, long layer_len,
-                        int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s) {
+                        int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s,
+                        double* final_out) {
   dim3 grid(LCH, nlayers, 1);
   // CMG_CGS_UNROLL: strides per load batch of the fused CGS pass (8 launches at E=64^3:
   // 1 -> 10.3 ms at 3.6 TB/s, 2 -> 7.2 ms at 5.2 TB/s; profiles/r02/ab_dots.txt)
@@ -1685,9 +1717,7 @@ void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* 
   else if (nv <= 16) k_layer_cgs_dots<16><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   else k_layer_cgs_dots<32><<<grid, 256, 0, s>>>(V, ldv, nv, coef, w, layer_len, nlayers, hcol, hstride, partials);
   CMG_LAUNCH_CHECK();
-  const long t = (long)nv * nlayers;
-  k_layer_reduce<<<(unsigned)((t + 127) / 128), 128, 0, s>>>(partials, nv, nlayers, out);
-  CMG_LAUNCH_CHECK();
+  layer_reduce_launch(partials, nv, nlayers, out, final_out, 0, s);
 }
 
 void sem_layer_finalize(const double* gathered, int nv, const int* lpr, int nranks, double* out,

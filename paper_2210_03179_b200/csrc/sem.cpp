@@ -761,6 +761,10 @@ struct SemLevel final : cmg_op {
                     bool do_sqrt) {
     if (nv > 64) fail(CMG_EINVAL, "sem: too many vectors in one reduction");
     const long layer_len = static_cast<long>(Ex) * Ey * sem_nos(N);
+    if (!distributed() && Ezl <= 4096) {  // per-layer sums and their z-ordered total in one launch
+      sem_layer_dots(V, ldv, nv, w, layer_len, Ezl, lpart.p, lout.p, ctx->stream, out, do_sqrt ? 1 : 0);
+      return;
+    }
     sem_layer_dots(V, ldv, nv, w, layer_len, Ezl, lpart.p, lout.p, ctx->stream);
     const double* g = lout.p;
     if (distributed()) {
@@ -783,6 +787,10 @@ struct SemLevel final : cmg_op {
       return;
     }
     const long layer_len = static_cast<long>(Ex) * Ey * sem_nos(N);
+    if (!distributed() && Ezl <= 4096) {
+      sem_layer_cgs_dots(V, ldv, nv, coef_in, w, layer_len, Ezl, hcol, hstride, lpart.p, lout.p, ctx->stream, out);
+      return;
+    }
     sem_layer_cgs_dots(V, ldv, nv, coef_in, w, layer_len, Ezl, hcol, hstride, lpart.p, lout.p, ctx->stream);
     const double* g = lout.p;
     if (distributed()) {

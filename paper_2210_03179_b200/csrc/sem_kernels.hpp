@@ -130,11 +130,16 @@ void sem_restrict_local(const SemArgs& fine, int Nc, const double* J, const doub
                         double* Lc, cudaStream_t s);
 
 // per-layer partial inner products: out[v*Ezl + l] = sum over layer l of V_v . w
+// final_out != nullptr (one GPU, nlayers <= 4096): the per-layer sums and their
+// z-ordered total in one launch straight into final_out[v] (sqrt'ed if do_sqrt),
+// same bits as out + sem_layer_finalize
 void sem_layer_dots(const double* V, std::size_t ldv, int nv, const double* w, long layer_len,
-                    int nlayers, double* partials, double* out, cudaStream_t s);
+                    int nlayers, double* partials, double* out, cudaStream_t s, double* final_out = nullptr,
+                    int do_sqrt = 0);
 // fused CGS pass (nv <= 32): w -= V coef, hcol += coef, then the per-layer V^T w
 void sem_layer_cgs_dots(const double* V, std::size_t ldv, int nv, const double* coef, double* w, long layer_len,
-                        int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s);
+                        int nlayers, double* hcol, int hstride, double* partials, double* out, cudaStream_t s,
+                        double* final_out = nullptr);
 // final sum over all global layers (gathered [rank][v][layer_local] blocks) in z order
 void sem_layer_finalize(const double* gathered, int nv, const int* layers_per_rank, int nranks,
                         double* out, int do_sqrt, cudaStream_t s);
